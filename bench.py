@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the ARGUS per-batch routing path on B200 (prints ONE JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl argus|reference]
+
+A step = one pass of the whole hot path (K6 prep, K1/K2 scan + fused top-k, K5
+merges, K3 predictor + A5, K4 assignment) over one batch of synthetic input.
+At N=1 the workload is BASELINE.json configs[1] (C2): Twitter-trace-shaped
+bursty batches N=16..512 against an M=1M cache, d=768, k=4, L=12.
+
+value  = prompts routed per second, inputs already resident in HBM, timed with
+         CUDA events on the router's stream over exactly K steps (max over ranks).
+e2e    = the same metric through the host-buffer ABI call argus_route_batch
+         (pinned host prompts, H2D + D2H inside every step).
+roofline = the scan kernel (K1+K2): algorithmic cache bytes M*(2d+4) per launch
+         / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the fp64 oracle (oracle/, unchanged) on a bounded sample of the
+         same workload on this host's cores.
+--impl reference = the oracle as the reference arm (there is no reference code
+         to install: the paper publishes none).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import argus_inputs as gen  # noqa: E402
+
+N_TRACE = 256  # distinct batches generated from the MMPP trace, cycled over the steps
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="argus", choices=["argus", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def batch_sizes(cfg):
+    if cfg.bursty:
+        return gen.bursty_sizes(N_TRACE, seed=2018, lo=16, hi=cfg.N)
+    return [cfg.N] * N_TRACE
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling via NVML during the timed region."""
+
+    def __init__(self, device_index=0, period=0.02):
+        self.samples, self.reasons = [], set()
+        self.period = period
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                m = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, b in names.items():
+                    if m & b and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline(cfg, cache_rows, queries, opts, W1, b1, W2, b2, quota_fn, seconds):
+    """The oracle, as it stands, on a bounded sample: S prompts of the workload
+    scanned over the FULL cache (O1..O4), then O5 and O6..O10 on those prompts."""
+    import oracle
+    threads = oracle.max_threads()
+    # calibrate: one prompt over a 64K-row slice on all threads
+    probe = cache_rows[:65536]
+    t0 = time.perf_counter()
+    oracle.scan_topk(queries[:threads], probe, cfg.k, threads=threads)
+    dt = time.perf_counter() - t0
+    per_prompt_full = dt / threads * (cache_rows.shape[0] / probe.shape[0])  # wall s per prompt at full M
+    S = int(max(1, min(queries.shape[0], seconds / max(per_prompt_full, 1e-9))))
+    S = max(1, (S // threads) * threads) if S >= threads else S
+    X = queries[:S]
+    t0 = time.perf_counter()
+    sc, ix = oracle.scan_topk(X, cache_rows, cfg.k, threads=threads)
+    rh = oracle.mlp(X, sc, W1, b1, W2, b2, threads=threads)
+    oracle.assign(rh, sc[:, 0], opts, quota_fn(S))
+    wall = time.perf_counter() - t0
+    return {"value": S / wall, "unit": "prompts/s", "cores": threads, "kind": "oracle",
+            "sample": f"{S} prompts of the {cfg.name} workload scanned over the full M={cache_rows.shape[0]} cache "
+                      f"(fp64 C oracle, OpenMP over prompts), then predictor + assignment; {wall:.1f} s wall"}
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    cfg = gen.CONFIGS[args.config]
+    assert args.gpus == world or world == 1, "launch N>1 with torchrun --nproc-per-node N"
+    assert args.warmup >= 0 and args.steps >= 1
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2511_06724_b200 import argus
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    d, k = cfg.d, cfg.k
+    opts = gen.option_table(cfg.models, cfg.ks)
+    L = len(opts)
+    W1, b1, W2, b2 = gen.mlp_weights(d, k, cfg.hidden, L, stress=cfg.stress)
+    fr = gen.load_fractions(L, cfg.frac_base)
+    sizes = batch_sizes(cfg)
+    max_batch = max(sizes)
+
+    uid = None
+    if world > 1:
+        obj = [argus.argus_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()
+    r = argus.Router(d, k, opts, W1, b1, W2, b2, capacity=cfg.M, max_batch=max_batch, rank=rank, world=world,
+                     device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream)
+
+    # ---- cache: generated chunk by chunk, inserted through the ABI (rank 0 authoritative)
+    cg = gen.CacheGen(cfg.M, d, cfg.seed)
+    keep_rows = rank == 0 and not args.no_cpu_baseline
+    cache_rows = np.empty((cfg.M, d), np.float32) if keep_rows else None
+    t0 = time.perf_counter()
+    for a, chunk in cg.chunks():
+        if cache_rows is not None:
+            cache_rows[a:a + chunk.shape[0]] = chunk
+        r.argus_cache_insert(chunk)  # rank 0's rows are authoritative (broadcast by the library)
+    t_insert = time.perf_counter() - t0
+
+    # ---- batches (inputs resident in HBM for `value`; pinned host copies for e2e)
+    Xs = [gen.queries(cg, n, cfg.seed, b, cache_rows=cache_rows) for b, n in enumerate(sizes)]
+    quotas = [argus.argus_quota_from_fractions(fr, n) for n in sizes]
+    X_dev = [torch.from_numpy(x).to(f"cuda:{local_rank}") for x in Xs]
+    X_pin = [torch.from_numpy(x).pin_memory() for x in Xs]
+    dev = torch.device("cuda", local_rank)
+    out = dict(option=torch.empty(max_batch, dtype=torch.int32, device=dev),
+               topk_idx=torch.empty((max_batch, k), dtype=torch.int32, device=dev),
+               topk_score=torch.empty((max_batch, k), dtype=torch.float32, device=dev),
+               quality=torch.empty((max_batch, L), dtype=torch.float32, device=dev),
+               status=torch.empty(max_batch, dtype=torch.uint8, device=dev))
+
+    def step(t):
+        b = t % N_TRACE
+        r.argus_route_batch_dev(X_dev[b], quotas[b], out["option"], out["topk_idx"], out["topk_score"],
+                                out["quality"], out["status"])
+        return sizes[b]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize()
+
+    for t in range(args.warmup):
+        step(t)
+    r.argus_sync()
+    r.argus_profile_read()  # reset
+    r.argus_profile_enable(True)
+    barrier()
+    launches0 = r.argus_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    prompts = 0
+    with sampler:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for t in range(args.warmup, args.warmup + args.steps):
+                prompts += step(t)
+            ev1.record(stream)
+        ev1.synchronize()
+    rc = r.argus_sync()
+    launches = r.argus_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    prof = r.argus_profile_read()
+    r.argus_profile_enable(False)
+    barrier()
+    ms_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    total_prompts = prompts  # every rank routes the same prompts; the batch is the job's unit
+    value = total_prompts / (ms_max / 1e3)
+
+    # ---- e2e through the host-buffer ABI call
+    e2e_steps = args.e2e_steps or min(args.steps, 200)
+    Xh = [x.numpy() for x in X_pin]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e2e_prompts, h2d, d2h = 0, 0, 0
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for t in range(e2e_steps):
+            b = t % N_TRACE
+            r.argus_route_batch(Xh[b], quotas[b])
+            n = sizes[b]
+            e2e_prompts += n
+            h2d += n * d * 4
+            d2h += n * (4 + k * 8 + L * 4 + 1)
+        e1.record(stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    # ---- roofline of the dominant kernel (the scan)
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
+    scan_ms, scan_n = prof["scan"]
+    m_local = (cfg.M + world - 1) // world
+    bytes_per_launch = m_local * (2 * d + 4)
+    achieved_gbs = bytes_per_launch * scan_n / (scan_ms / 1e3) / 1e9 if scan_n else None
+    flops = sum(2.0 * sizes[t % N_TRACE] * m_local * d for t in range(args.warmup, args.warmup + args.steps))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+    stage_ms = {kk: round(v[0] / max(1, args.steps), 5) for kk, v in prof.items() if v[1]}
+    total_stage = sum(v[0] for v in prof.values())
+
+    res = {
+        "metric": "prompts routed/sec (per-batch approximation-level routing: cosine cache scan + top-k + "
+                  "quality predictor + quota assignment)",
+        "value": round(value, 1),
+        "unit": "prompts/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 5),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{cfg.name}: {cfg.note}",
+            "M": cfg.M, "d": d, "k": k, "L": L, "hidden": cfg.hidden,
+            "batch_sizes": f"MMPP trace seed 2018, {N_TRACE} batches cycled, mean N {np.mean(sizes):.1f}, "
+                           f"min {min(sizes)}, max {max(sizes)}" if cfg.bursty else f"N={cfg.N}",
+            "parallelism": f"cache row-striped over {world} GPU(s)",
+            "l2": f"inputs larger than L2 (cache shard {bytes_per_launch / 1e9:.2f} GB >> 126 MB L2)",
+            "insert_s": round(t_insert, 2),
+        },
+        "e2e": {"value": round(e2e_prompts / (e2e_ms / 1e3), 1), "unit": "prompts/s",
+                "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
+                "steps": e2e_steps, "api": "argus_route_batch (host buffers)"},
+        "gpu_launches": int(launches),
+        "roofline": {
+            "kernel": "scan (K1+K2 fused cosine scan + top-k)",
+            "bound": "hbm",
+            "achieved": round(achieved_gbs, 1) if achieved_gbs else None,
+            "peak": hbm,
+            "unit": "GB/s",
+            "frac": round(achieved_gbs / hbm, 4) if achieved_gbs else None,
+            "traffic": traffic,
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "scan_ms_per_launch": round(scan_ms / max(1, scan_n), 5),
+            "scan_share_of_step": round(scan_ms / max(total_stage, 1e-9), 4),
+            "tensor_tflops_achieved": round(flops / (scan_ms / 1e3) / 1e12, 2) if scan_ms else None,
+            "tensor_peak_tflops": tf_sust,
+        },
+        "stage_ms_per_step": stage_ms,
+        "route_rc": rc,
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, cache_rows, np.concatenate(Xs[:8]), opts, W1, b1, W2, b2,
+                                           lambda n: gen_quota(fr, n), args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def gen_quota(fr, n):
+    import oracle
+    return oracle.quota_from_fractions(fr, n)
+
+
+def run_reference(args, cfg, rank, world):
+    """Reference arm = the fp64 oracle as it stands, on this host's cores.  Each
+    step routes a bounded sample of one batch of the workload over the full cache."""
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    d, k = cfg.d, cfg.k
+    opts = gen.option_table(cfg.models, cfg.ks)
+    L = len(opts)
+    W1, b1, W2, b2 = gen.mlp_weights(d, k, cfg.hidden, L, stress=cfg.stress)
+    fr = gen.load_fractions(L, cfg.frac_base)
+    cg = gen.CacheGen(cfg.M, d, cfg.seed)
+    cache_rows = cg.all()
+    sizes = batch_sizes(cfg)
+    threads = oracle.max_threads()
+    # sample per step sized so that the whole run stays within a few minutes
+    probe = cache_rows[:65536]
+    q0 = gen.queries(cg, threads, cfg.seed, 0, cache_rows=cache_rows)
+    t0 = time.perf_counter()
+    oracle.scan_topk(q0, probe, k, threads=threads)
+    per_prompt = (time.perf_counter() - t0) / threads * (cfg.M / 65536)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    S = max(1, int(budget / max(per_prompt, 1e-9)))
+    S = max(threads, (S // threads) * threads) if S >= threads else S
+    total_ms, prompts = 0.0, 0
+    for t in range(args.warmup + args.steps):
+        b = t % N_TRACE
+        n = min(S, sizes[b])
+        X = gen.queries(cg, sizes[b], cfg.seed, b, cache_rows=cache_rows)[:n]
+        t1 = time.perf_counter()
+        sc, ix = oracle.scan_topk(X, cache_rows, k, threads=threads)
+        rh = oracle.mlp(X, sc, W1, b1, W2, b2, threads=threads)
+        oracle.assign(rh, sc[:, 0], opts, oracle.quota_from_fractions(fr, n))
+        dt = (time.perf_counter() - t1) * 1e3
+        if t >= args.warmup:
+            total_ms += dt
+            prompts += n
+    value = prompts / (total_ms / 1e3)
+    res = {
+        "impl": "reference",
+        "metric": "prompts routed/sec (per-batch approximation-level routing: cosine cache scan + top-k + "
+                  "quality predictor + quota assignment)",
+        "value": round(value, 3), "unit": "prompts/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.note}", "M": cfg.M, "d": d, "k": k, "L": L,
+                   "sample_per_step": f"first min({S}, N_b) prompts of each trace batch over the full cache"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "prompts/s", "cores": threads, "kind": "oracle",
+                         "sample": f"<= {S} prompts per step over the full M={cfg.M} cache"},
+        "e2e": {"value": round(value, 3), "unit": "prompts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "no reference implementation exists (the paper publishes no code); the reference arm is the "
+                "fp64 CPU oracle written from the paper",
+    }
+    print(json.dumps(res), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -1,0 +1,229 @@
+/*
+ * argus.h -- C ABI of libargus.so, the B200 (sm_100a) per-batch
+ * approximation-level router of ARGUS (arXiv 2511.06724).
+ *
+ * For a batch of N prompt embeddings the library runs the hot path of
+ * SURVEY.md §8(a) entirely in its own CUDA kernels:
+ *   A1 query preparation  fp32 -> bf16, inverse norms
+ *   A2 cache scan         cosine S = <x, c> / (|x| |c|)           (§2.1 "Using similarity
+ *                         search, the most similar cached prompt is retrieved"; §4.5; §4.7)
+ *   A3 top-k              k best (score desc, global id asc); the N x M score
+ *                         matrix never reaches HBM                 ("most similar")
+ *   A4 quality predictor  r = sigmoid(W2 relu(W1 [x; s] + b1) + b2), r_0 := 1
+ *                                                                  (§4.1, §4.4)
+ *   A5 compliance         A_i = {v : v = 0 or k_skip_v = 0 or s_i1 >= tau_v},
+ *                         C_i = {v in A_i : r_iv >= delta}, delta = 0.9 (§3),
+ *                         preference pi_i = A_i by (r desc, p_th desc, v asc),
+ *                         priority (|C_i| asc, i asc)
+ *   A6 assignment         serial dictatorship under per-option integer quotas c_v
+ *                         derived from the allocator's F(v)     (Eq. 1, §4.3)
+ * The numbered readings of the paper (ties, >= vs >, gates, overflow) are listed
+ * in DESIGN.md §"Readings".
+ *
+ * Conventions (all functions):
+ *   - return 0 (ARGUS_OK) on success, > 0 for a warning, < 0 for an error;
+ *     no exceptions cross the ABI;
+ *   - the caller owns every array it passes; the library copies what it needs
+ *     (cache rows, weights, option table) into its own device memory and never
+ *     retains a caller pointer past the call;
+ *   - "host" pointers are ordinary (pageable or pinned) CPU memory; "dev"
+ *     pointers are CUDA device memory on cfg.device;
+ *   - after a CUDA or NCCL failure the router is poisoned and every later call
+ *     on it returns ARGUS_E_STATE (argus_route_destroy still frees it);
+ *   - a router is not thread-safe: one router per thread / process.
+ *
+ * Multi-GPU (world > 1, one process per GPU): the cache is row-striped, global
+ * id g lives on rank g mod world at local slot g div world.  argus_cache_insert
+ * and argus_route_batch* are collectives (every rank calls them in the same
+ * order).  With an NCCL unique id, rank 0's inputs are authoritative (other
+ * ranks may pass NULL inputs) and are broadcast by the library; the per-shard
+ * top-k candidates are exchanged with one all-gather of N*k u64 keys.  Without
+ * a unique id ("external" mode) every rank passes the same inputs and the
+ * caller moves the keys between argus_route_partial_dev and
+ * argus_route_finish_dev itself.  Outputs are identical on every rank.
+ */
+#ifndef ARGUS_H
+#define ARGUS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ------------------------------------------------------------ return codes */
+#define ARGUS_OK 0
+#define ARGUS_W_OVERFLOW 1        /* some prompt found no admissible quota; it got option 0 */
+#define ARGUS_E_INVALID (-1)      /* bad argument, non-finite value or zero-norm vector   */
+#define ARGUS_E_CAPACITY (-2)     /* an insert would exceed cfg.capacity                  */
+#define ARGUS_E_CUDA (-3)         /* CUDA runtime / launch failure (router poisoned)      */
+#define ARGUS_E_NCCL (-4)         /* NCCL failure (router poisoned)                       */
+#define ARGUS_E_STATE (-5)        /* router poisoned, or call not valid in this mode      */
+#define ARGUS_E_UNIMPLEMENTED (-6)
+
+/* per-prompt status bits (status_out) */
+#define ARGUS_ST_OVERFLOW 1u      /* no option of pi_i had quota left -> option 0          */
+#define ARGUS_ST_NONCOMPLIANT 2u  /* assigned option has r < delta                         */
+#define ARGUS_ST_GATED_ALL 4u     /* every gated (k_skip > 0) option failed its gate (miss) */
+
+typedef struct argus_router argus_router; /* opaque, owned by the library */
+
+/* One approximation option v (SPEC S:26-32 Variant).
+ * The table passed to argus_route_init is ordered slow -> fast: option 0
+ * is the full model (k_skip must be 0), p_th_qpm must be non-decreasing.
+ *   model_id  caller's model identifier (metadata only)
+ *   k_skip    approximate-caching skip level K, 0 <= K < 50 (T = 50)
+ *   p_th_qpm  peak throughput P_th(v) in queries/minute (used for tie-breaks)
+ *   sim_gate  tau_v: option admissible only if the top-1 cosine >= tau_v
+ *             (ignored, i.e. -inf, when k_skip == 0; "based on prompt
+ *             similarity, an appropriate approximation level (K) is selected") */
+typedef struct {
+  int32_t model_id;
+  int32_t k_skip;
+  float p_th_qpm;
+  float sim_gate;
+} argus_option;
+
+/* Router configuration.
+ *   d          embedding dimension, multiple of 64, 64 <= d <= 768 (CLIP d=768)
+ *   k          top-k, 1 <= k <= 8
+ *   L          number of options, 1 <= L <= 32
+ *   hidden     predictor hidden width H, multiple of 32, 32 <= H <= 1024
+ *   max_batch  largest N a route call may pass, 1 <= max_batch <= 8192
+ *   capacity   max global cache entries, capacity <= 2^32 - 2
+ *   delta      optimal-quality threshold (0.9); compared as float r >= delta
+ *   rank, world, device   this process's rank, world size (1 = single GPU), CUDA device
+ *   nccl_unique_id        128-byte ncclUniqueId identical on all ranks, or NULL
+ *                         (world == 1, or external collective mode)
+ *   stream     cudaStream_t to run on, or NULL (the library creates one) */
+typedef struct {
+  int32_t d, k, L, hidden;
+  int32_t max_batch;
+  int64_t capacity;
+  float delta;
+  int32_t rank, world, device;
+  const void* nccl_unique_id;
+  void* stream;
+} argus_config;
+
+/* Create an ncclUniqueId (128 bytes) on rank 0; share it with the other ranks
+ * (e.g. torch.distributed.broadcast_object_list) before argus_route_init. */
+int argus_nccl_unique_id(void* out128);
+
+/* Create a router.  Host arrays (copied):
+ *   opts [L]                 option table, slow -> fast
+ *   w1 [hidden][d + k] fp32  layer-1 weights; columns [0, d) act on the prompt
+ *                            embedding and are stored as bf16 (RNE; the canonical
+ *                            tensor-core operand), columns [d, d+k) act on the
+ *                            top-k cosine scores (fp32)
+ *   b1 [hidden], w2 [L][hidden], b2 [L]  fp32
+ * Errors: ARGUS_E_INVALID (ranges above, opts[0].k_skip != 0, k_skip outside
+ * [0,50), p_th decreasing, non-finite weights), ARGUS_E_CUDA, ARGUS_E_NCCL.
+ * With world > 1 and a unique id this is a collective; rank 0's opts/weights are
+ * broadcast (others may pass NULL). */
+int argus_route_init(const argus_config* cfg, const argus_option* opts, const float* w1,
+                     const float* b1, const float* w2, const float* b2, argus_router** out);
+
+/* Append n cache entries (host fp32 [n][d], row-major) with global ids
+ * [M, M + n); *first_id (may be NULL) receives M.  Each row is stored as bf16
+ * (RNE) with an fp32 inverse norm of the stored values.  Errors:
+ * ARGUS_E_INVALID (non-finite value or zero-norm row; the cache is unchanged),
+ * ARGUS_E_CAPACITY.  Collective when world > 1. */
+int argus_cache_insert(argus_router* r, const float* emb, int64_t n, int64_t* first_id);
+
+/* Same, rows already on the device (fp32 [n][d]); synchronous. */
+int argus_cache_insert_dev(argus_router* r, const float* emb_dev, int64_t n, int64_t* first_id);
+
+/* Route one batch (host buffers; synchronous).
+ *   prompts [N][d] fp32 host, 1 <= N <= max_batch
+ *   quota [L] int32 host, quota[v] >= 0 (sum >= N expected; otherwise the
+ *         overflowing prompts get option 0 and ARGUS_ST_OVERFLOW)
+ * Outputs (host, caller-allocated):
+ *   option_out [N] int32    assigned option index
+ *   topk_idx [N][k] uint32  global cache ids, best first (0xFFFFFFFF pads M < k)
+ *   topk_score [N][k] fp32  cosine scores, best first (-1.0 pads)
+ *   quality_out [N][L] fp32 predicted relative quality r, or NULL
+ *   status_out [N] uint8    ARGUS_ST_* bits, or NULL
+ * Returns ARGUS_OK, ARGUS_W_OVERFLOW, or an error (ARGUS_E_INVALID for a
+ * non-finite / zero-norm prompt or a negative quota). */
+int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                      int32_t* option_out, uint32_t* topk_idx, float* topk_score,
+                      float* quality_out, uint8_t* status_out);
+
+/* Device-buffer variant: prompts_dev fp32 [N][d] and the outputs are device
+ * pointers (quality_dev, status_dev may be NULL); quota is a HOST int32 [L].
+ * Enqueued asynchronously on the router's stream; returns ARGUS_OK once
+ * enqueued.  Value errors found on the device (invalid prompt) and the
+ * overflow warning are reported by the next argus_sync(). */
+int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N,
+                          const int32_t* quota, int32_t* option_out_dev,
+                          uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
+                          uint8_t* status_dev);
+
+/* Sharded pipeline pieces (external collective mode and tests).
+ * partial: A1-A3 on this rank's shard -> keys_dev [N][k] uint64 (sorted desc;
+ *          key = ord(score) << 32 | (0xFFFFFFFF - g), 0 = empty).
+ * finish:  merge G shards' keys (keys_all_dev [G][N][k]) -> A3 outputs, then
+ *          A4-A6 exactly as argus_route_batch_dev.  prompts_dev must be the
+ *          same batch passed to partial (its bf16 copy is reused). */
+int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N,
+                            uint64_t* keys_dev);
+int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
+                           const int32_t* quota, int32_t* option_out_dev,
+                           uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
+                           uint8_t* status_dev);
+
+/* Wait for the router's stream; return the deferred code of the enqueued work
+ * (ARGUS_OK, ARGUS_W_OVERFLOW, ARGUS_E_INVALID) and clear it. */
+int argus_sync(argus_router* r);
+
+/* Largest-remainder integer quotas from load shares (host helper, O(L)):
+ * t_v = (f_v * N) / S with S = sum_v f_v summed v = 0..L-1 in double;
+ * c_v = floor(t_v); the N - sum c leftover units go one each to the largest
+ * fractional parts t_v - c_v, ties to the lower v.  sum c = N.
+ * f [L] >= 0 finite with S > 0, 1 <= L <= 64, N >= 0; c_out [L]. */
+int argus_quota_from_fractions(const double* f, int32_t L, int32_t N, int32_t* c_out);
+
+/* Number of cache entries inserted so far (global, identical on all ranks). */
+int argus_cache_size(const argus_router* r, int64_t* m_out);
+
+/* Number of kernel launches the router has issued so far (for bench accounting). */
+int argus_launch_count(const argus_router* r, int64_t* n_out);
+
+/* The router's CUDA stream (cudaStream_t as void*). */
+int argus_get_stream(const argus_router* r, void** stream_out);
+
+/* Per-stage kernel timing (measurement only).  When enabled, the library
+ * records a CUDA event pair on its stream around every kernel it launches;
+ * argus_profile_read synchronises and returns, for one stage, the summed
+ * device milliseconds and the number of launches since the last read (then
+ * resets that stage).  Stages: 0 prep (K6), 1 scan (K1+K2), 2 merge over CTA
+ * ranges (K5), 3 merge over shards (K5), 4 predictor (K3+A5), 5 assignment (K4),
+ * 6 insert (K0). */
+#define ARGUS_STAGE_PREP 0
+#define ARGUS_STAGE_SCAN 1
+#define ARGUS_STAGE_MERGE_LOCAL 2
+#define ARGUS_STAGE_MERGE_GLOBAL 3
+#define ARGUS_STAGE_MLP 4
+#define ARGUS_STAGE_ASSIGN 5
+#define ARGUS_STAGE_INSERT 6
+#define ARGUS_NUM_STAGES 7
+int argus_profile_enable(argus_router* r, int on);
+int argus_profile_read(argus_router* r, int stage, double* total_ms, int64_t* launches);
+
+/* Free all device memory, the NCCL communicator and the router. */
+int argus_route_destroy(argus_router* r);
+
+/* Static description of a return code. */
+const char* argus_strerror(int code);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARGUS_H */

@@ -1,0 +1,256 @@
+"""Thin ctypes binding of libargus.so (include/argus.h), same names as the C ABI.
+
+Argument marshalling only: every step of the routing path runs in the CUDA
+kernels of libargus.so.  PyTorch is used by callers for device memory, streams
+and process groups; this module accepts numpy arrays (host calls) or torch CUDA
+tensors (``*_dev`` calls) and passes raw pointers.  If the shared library is
+missing the import fails loudly -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libargus.so")
+
+ARGUS_OK = 0
+ARGUS_W_OVERFLOW = 1
+ARGUS_E_INVALID = -1
+ARGUS_E_CAPACITY = -2
+ARGUS_E_CUDA = -3
+ARGUS_E_NCCL = -4
+ARGUS_E_STATE = -5
+ARGUS_E_UNIMPLEMENTED = -6
+ST_OVERFLOW, ST_NONCOMPLIANT, ST_GATED_ALL = 1, 2, 4
+
+# every symbol include/argus.h declares
+SYMBOLS = (
+    "argus_nccl_unique_id", "argus_route_init", "argus_cache_insert", "argus_cache_insert_dev",
+    "argus_route_batch", "argus_route_batch_dev", "argus_route_partial_dev", "argus_route_finish_dev",
+    "argus_sync", "argus_quota_from_fractions", "argus_cache_size", "argus_launch_count",
+    "argus_get_stream", "argus_profile_enable", "argus_profile_read", "argus_route_destroy",
+    "argus_strerror",
+)
+STAGES = ("prep", "scan", "merge_local", "merge_global", "mlp", "assign", "insert")
+
+
+class argus_option(C.Structure):
+    _fields_ = [("model_id", C.c_int32), ("k_skip", C.c_int32),
+                ("p_th_qpm", C.c_float), ("sim_gate", C.c_float)]
+
+
+class argus_config(C.Structure):
+    _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("L", C.c_int32), ("hidden", C.c_int32),
+                ("max_batch", C.c_int32), ("capacity", C.c_int64), ("delta", C.c_float),
+                ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p)]
+
+
+class ArgusError(RuntimeError):
+    def __init__(self, code, what=""):
+        self.code = code
+        super().__init__(f"{what}: argus error {code}: {strerror(code)}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2511_06724_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "argus_nccl_unique_id": [P],
+        "argus_route_init": [P, P, P, P, P, P, P],
+        "argus_cache_insert": [P, P, I64, P],
+        "argus_cache_insert_dev": [P, P, I64, P],
+        "argus_route_batch": [P, P, I32, P, P, P, P, P, P],
+        "argus_route_batch_dev": [P, P, I32, P, P, P, P, P, P],
+        "argus_route_partial_dev": [P, P, I32, P],
+        "argus_route_finish_dev": [P, P, I32, I32, P, P, P, P, P, P],
+        "argus_sync": [P],
+        "argus_quota_from_fractions": [P, I32, I32, P],
+        "argus_cache_size": [P, P],
+        "argus_launch_count": [P, P],
+        "argus_get_stream": [P, P],
+        "argus_profile_enable": [P, C.c_int],
+        "argus_profile_read": [P, C.c_int, P, P],
+        "argus_route_destroy": [P],
+        "argus_strerror": [C.c_int],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    lib.argus_strerror.restype = C.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def strerror(code: int) -> str:
+    return _lib.argus_strerror(int(code)).decode()
+
+
+def _p(a):
+    """Raw pointer of a numpy array or a torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(C.c_void_p)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+def _check(rc, what):
+    if rc < 0:
+        raise ArgusError(rc, what)
+    return rc
+
+
+# ------------------------------------------------------------------ raw ABI (same names)
+def argus_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.argus_nccl_unique_id(buf), "argus_nccl_unique_id")
+    return buf.raw
+
+
+def argus_quota_from_fractions(f, N: int) -> np.ndarray:
+    f = np.ascontiguousarray(f, np.float64)
+    c = np.empty(f.size, np.int32)
+    _check(_lib.argus_quota_from_fractions(_p(f), f.size, int(N), _p(c)), "argus_quota_from_fractions")
+    return c
+
+
+def argus_strerror(code: int) -> str:
+    return strerror(code)
+
+
+class Router:
+    """Owner of one ``argus_router*``.  Methods map 1:1 onto the C ABI."""
+
+    def __init__(self, d, k, opts, W1, b1, W2, b2, capacity, max_batch, hidden=None,
+                 delta=0.9, rank=0, world=1, device=0, nccl_unique_id=None, stream=None):
+        L = len(opts)
+        self.d, self.k, self.L = int(d), int(k), L
+        W1 = np.ascontiguousarray(W1, np.float32)
+        H = W1.shape[0] if hidden is None else int(hidden)
+        self.H = H
+        self.max_batch = int(max_batch)
+        oa = (argus_option * L)()
+        for i, o in enumerate(opts):
+            oa[i] = argus_option(int(o["model_id"]), int(o["k_skip"]), float(o["p_th_qpm"]),
+                                 float(o["sim_gate"]))
+        self._uid = None
+        if nccl_unique_id is not None:
+            self._uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
+        cfg = argus_config(self.d, self.k, L, H, self.max_batch, int(capacity), float(delta),
+                           int(rank), int(world), int(device),
+                           C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
+                           C.c_void_p(stream) if stream else None)
+        self._keep = [np.ascontiguousarray(x, np.float32) for x in (W1, b1, W2, b2)]
+        h = C.c_void_p()
+        _check(_lib.argus_route_init(C.byref(cfg), oa, *[_p(x) for x in self._keep], C.byref(h)),
+               "argus_route_init")
+        self._h = h
+
+    # lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.argus_route_destroy(self._h)
+            self._h = None
+
+    argus_route_destroy = close
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # cache
+    def argus_cache_insert(self, emb) -> int:
+        emb = np.ascontiguousarray(emb, np.float32)
+        first = C.c_int64(-1)
+        _check(_lib.argus_cache_insert(self._h, _p(emb), emb.shape[0] if emb.size else 0, C.byref(first)),
+               "argus_cache_insert")
+        return first.value
+
+    def argus_cache_insert_dev(self, emb_dev) -> int:
+        first = C.c_int64(-1)
+        _check(_lib.argus_cache_insert_dev(self._h, _p(emb_dev), int(emb_dev.shape[0]), C.byref(first)),
+               "argus_cache_insert_dev")
+        return first.value
+
+    def argus_cache_size(self) -> int:
+        m = C.c_int64()
+        _check(_lib.argus_cache_size(self._h, C.byref(m)), "argus_cache_size")
+        return m.value
+
+    def argus_launch_count(self) -> int:
+        n = C.c_int64()
+        _check(_lib.argus_launch_count(self._h, C.byref(n)), "argus_launch_count")
+        return n.value
+
+    def argus_get_stream(self) -> int:
+        s = C.c_void_p()
+        _check(_lib.argus_get_stream(self._h, C.byref(s)), "argus_get_stream")
+        return s.value or 0
+
+    # routing
+    def argus_route_batch(self, prompts, quota, want_quality=True, want_status=True):
+        """Host-buffer route.  Returns (rc, dict of numpy outputs)."""
+        prompts = np.ascontiguousarray(prompts, np.float32)
+        quota = np.ascontiguousarray(quota, np.int32)
+        N = prompts.shape[0]
+        out = dict(option=np.empty(N, np.int32), topk_idx=np.empty((N, self.k), np.uint32),
+                   topk_score=np.empty((N, self.k), np.float32),
+                   quality=np.empty((N, self.L), np.float32) if want_quality else None,
+                   status=np.empty(N, np.uint8) if want_status else None)
+        rc = _check(_lib.argus_route_batch(self._h, _p(prompts), N, _p(quota), _p(out["option"]),
+                                           _p(out["topk_idx"]), _p(out["topk_score"]), _p(out["quality"]),
+                                           _p(out["status"])), "argus_route_batch")
+        return rc, out
+
+    def argus_route_batch_dev(self, prompts_dev, quota, option, topk_idx, topk_score, quality=None,
+                              status=None, N=None):
+        quota = np.ascontiguousarray(quota, np.int32)
+        N = int(prompts_dev.shape[0]) if N is None else int(N)
+        return _check(_lib.argus_route_batch_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
+                                                 _p(topk_idx), _p(topk_score), _p(quality), _p(status)),
+                      "argus_route_batch_dev")
+
+    def argus_route_partial_dev(self, prompts_dev, keys_dev, N=None):
+        N = int(prompts_dev.shape[0]) if N is None else int(N)
+        return _check(_lib.argus_route_partial_dev(self._h, _p(prompts_dev), N, _p(keys_dev)),
+                      "argus_route_partial_dev")
+
+    def argus_route_finish_dev(self, keys_all_dev, G, N, quota, option, topk_idx, topk_score,
+                               quality=None, status=None):
+        quota = np.ascontiguousarray(quota, np.int32)
+        return _check(_lib.argus_route_finish_dev(self._h, _p(keys_all_dev), int(G), int(N), _p(quota),
+                                                  _p(option), _p(topk_idx), _p(topk_score), _p(quality),
+                                                  _p(status)), "argus_route_finish_dev")
+
+    def argus_profile_enable(self, on=True):
+        _check(_lib.argus_profile_enable(self._h, int(bool(on))), "argus_profile_enable")
+
+    def argus_profile_read(self):
+        """{stage: (total_ms, launches)} since the last read (resets)."""
+        out = {}
+        for i, name in enumerate(STAGES):
+            ms, n = C.c_double(), C.c_int64()
+            _check(_lib.argus_profile_read(self._h, i, C.byref(ms), C.byref(n)), "argus_profile_read")
+            out[name] = (ms.value, n.value)
+        return out
+
+    def argus_sync(self) -> int:
+        return _check(_lib.argus_sync(self._h), "argus_sync")

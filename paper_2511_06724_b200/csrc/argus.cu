@@ -1,0 +1,760 @@
+// argus.cu -- host side of libargus.so: the C ABI declared in include/argus.h.
+//
+// Owns device memory, the CUDA stream, the NCCL communicator and the launch
+// sequence of one routing batch:
+//   K6 prep -> [NCCL broadcast of the batch when world > 1]
+//   -> K1/K2 fused scan + top-k -> K5 merge (CTA ranges)
+//   -> [NCCL all-gather of N*k keys] -> K5 merge (shards)
+//   -> K3 predictor + A5 -> K4 assignment.
+// No compute happens on the host: every step of the path is a kernel in this
+// library; the host validates arguments, moves buffers and launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/argus.h"
+#include "kernels.h"
+
+using namespace argus;
+
+namespace {
+
+constexpr int64_t INSERT_CHUNK = 1 << 16;  // rows per staged insert chunk
+
+struct QuotaArg {
+  int32_t c[32];
+};
+
+// NCCL is resolved lazily with dlopen (reusing an already-loaded libnccl.so.2,
+// e.g. torch's) so that loading libargus never pins a second NCCL into a process.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.tried) {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (h) {
+#define NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+      NCCL_SYM(GetUniqueId); NCCL_SYM(CommInitRank); NCCL_SYM(CommDestroy); NCCL_SYM(Broadcast);
+      NCCL_SYM(AllGather); NCCL_SYM(AllReduce); NCCL_SYM(GroupStart); NCCL_SYM(GroupEnd);
+      NCCL_SYM(GetErrorString);
+#undef NCCL_SYM
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.AllGather &&
+               api.AllReduce && api.GroupStart && api.GroupEnd && api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+}  // namespace
+
+struct argus_router {
+  argus_config cfg{};
+  int num_sms = 148;
+  bool own_stream = false;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  bool poisoned = false;
+  int64_t m_global = 0;   // entries inserted (all ranks agree)
+  int64_t cap_local = 0;  // rows allocated in this shard
+  int64_t launches = 0;
+  int32_t n_pad_max = 0;
+  int32_t p_max = 0;
+  // options (device)
+  int32_t* d_kskip = nullptr;
+  float* d_pth = nullptr;
+  float* d_gate = nullptr;
+  // weights (device)
+  __nv_bfloat16* d_W1xT = nullptr;
+  float* d_W1sT = nullptr;
+  float* d_b1 = nullptr;
+  float* d_W2T = nullptr;
+  float* d_b2 = nullptr;
+  // cache shard (device)
+  __nv_bfloat16* d_Cb = nullptr;
+  float* d_invc = nullptr;
+  // per-batch workspace (device)
+  float* d_Xstage = nullptr;       // [max(max_batch, INSERT_CHUNK)][d] fp32 staging
+  __nv_bfloat16* d_Xb = nullptr;   // [n_pad_max][d]
+  float* d_invq = nullptr;         // [n_pad_max]
+  uint64_t* d_partial = nullptr;   // [p_max][max_batch][k]
+  uint64_t* d_keys = nullptr;      // [max_batch][k]
+  uint64_t* d_keys_all = nullptr;  // [world][max_batch][k]
+  float* d_score = nullptr;        // [max_batch][k]
+  uint32_t* d_idx = nullptr;       // [max_batch][k]
+  float* d_rhat = nullptr;         // [max_batch][L]
+  uint8_t* d_pref = nullptr;       // [max_batch][L]
+  uint8_t* d_ccount = nullptr;     // [max_batch]
+  uint32_t* d_cmask = nullptr;     // [max_batch]
+  uint8_t* d_status = nullptr;     // [max_batch]
+  int32_t* d_option = nullptr;     // [max_batch]
+  int32_t* d_order = nullptr;      // [max_batch]
+  uint32_t* d_flags = nullptr;     // error / overflow flags
+  uint32_t* h_flags = nullptr;     // pinned mirror
+  // stage profiling (argus_profile_*)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;  // (stage, (start, stop))
+  double prof_ms[ARGUS_NUM_STAGES] = {};
+  int64_t prof_n[ARGUS_NUM_STAGES] = {};
+};
+
+// ------------------------------------------------------------------ helpers
+#define CU_TRY(r, expr)                                               \
+  do {                                                                \
+    cudaError_t _e = (expr);                                          \
+    if (_e != cudaSuccess) {                                          \
+      if (getenv("ARGUS_DEBUG"))                                      \
+        fprintf(stderr, "argus: %s -> %s\n", #expr, cudaGetErrorString(_e)); \
+      (r)->poisoned = true;                                           \
+      return ARGUS_E_CUDA;                                            \
+    }                                                                 \
+  } while (0)
+
+#define NC_TRY(r, expr)                                               \
+  do {                                                                \
+    ncclResult_t _e = (expr);                                         \
+    if (_e != ncclSuccess) {                                          \
+      if (getenv("ARGUS_DEBUG"))                                      \
+        fprintf(stderr, "argus: %s -> %s\n", #expr, nccl().GetErrorString(_e)); \
+      (r)->poisoned = true;                                           \
+      return ARGUS_E_NCCL;                                            \
+    }                                                                 \
+  } while (0)
+
+#define LAUNCHED(r)                                                   \
+  do {                                                                \
+    (r)->launches++;                                                  \
+    CU_TRY(r, cudaGetLastError());                                    \
+  } while (0)
+
+template <class T>
+static int dalloc(argus_router* r, T** p, size_t n) {
+  if (n == 0) n = 1;
+  CU_TRY(r, cudaMalloc((void**)p, n * sizeof(T)));
+  return ARGUS_OK;
+}
+
+static bool nccl_mode(const argus_router* r) { return r->cfg.world > 1 && r->comm != nullptr; }
+
+// transpose / round the predictor weights on the device (init time)
+__global__ void k_prep_weights(const float* __restrict__ w1, const float* __restrict__ w2, int d, int k,
+                               int H, int L, __nv_bfloat16* __restrict__ W1xT, float* __restrict__ W1sT,
+                               float* __restrict__ W2T) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = (int64_t)H * (d + k);
+  if (tid < n1) {
+    const int j = (int)(tid / (d + k)), c = (int)(tid % (d + k));
+    const float w = w1[tid];
+    if (c < d) W1xT[(int64_t)c * H + j] = __float2bfloat16_rn(w);
+    else W1sT[(int64_t)(c - d) * H + j] = w;
+  } else if (tid < n1 + (int64_t)L * H) {
+    const int64_t t = tid - n1;
+    const int v = (int)(t / H), j = (int)(t % H);
+    W2T[(int64_t)j * L + v] = w2[t];
+  }
+}
+
+static int finite_all(const float* p, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return 0;
+  return 1;
+}
+
+static int check_state(const argus_router* r) {
+  if (!r) return ARGUS_E_INVALID;
+  if (r->poisoned) return ARGUS_E_STATE;
+  return ARGUS_OK;
+}
+
+static cudaEvent_t ev_get(argus_router* r) {
+  if (!r->ev_pool.empty()) {
+    cudaEvent_t e = r->ev_pool.back();
+    r->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Bracket one kernel launch with an event pair when profiling is on.
+struct StageScope {
+  argus_router* r;
+  int stage;
+  cudaEvent_t a = nullptr, b = nullptr;
+  StageScope(argus_router* r_, int st) : r(r_), stage(st) {
+    if (r->prof) {
+      a = ev_get(r);
+      b = ev_get(r);
+      cudaEventRecord(a, r->stream);
+    }
+  }
+  ~StageScope() {
+    if (r->prof && a && b) {
+      cudaEventRecord(b, r->stream);
+      r->ev_open.push_back({stage, {a, b}});
+    }
+  }
+};
+
+static void prof_collect(argus_router* r) {
+  if (r->ev_open.empty()) return;
+  cudaStreamSynchronize(r->stream);
+  for (auto& x : r->ev_open) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, x.second.first, x.second.second) == cudaSuccess) {
+      r->prof_ms[x.first] += ms;
+      r->prof_n[x.first] += 1;
+    }
+    r->ev_pool.push_back(x.second.first);
+    r->ev_pool.push_back(x.second.second);
+  }
+  r->ev_open.clear();
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int argus_profile_enable(argus_router* r, int on) {
+  if (!r) return ARGUS_E_INVALID;
+  cudaSetDevice(r->cfg.device);
+  prof_collect(r);
+  r->prof = on != 0;
+  return ARGUS_OK;
+}
+
+int argus_profile_read(argus_router* r, int stage, double* total_ms, int64_t* launches) {
+  if (!r || stage < 0 || stage >= ARGUS_NUM_STAGES) return ARGUS_E_INVALID;
+  cudaSetDevice(r->cfg.device);
+  prof_collect(r);
+  if (total_ms) *total_ms = r->prof_ms[stage];
+  if (launches) *launches = r->prof_n[stage];
+  r->prof_ms[stage] = 0.0;
+  r->prof_n[stage] = 0;
+  return ARGUS_OK;
+}
+
+const char* argus_strerror(int code) {
+  switch (code) {
+    case ARGUS_OK: return "ok";
+    case ARGUS_W_OVERFLOW: return "warning: some prompt found no admissible quota (assigned option 0)";
+    case ARGUS_E_INVALID: return "invalid argument, non-finite value or zero-norm vector";
+    case ARGUS_E_CAPACITY: return "cache capacity exceeded";
+    case ARGUS_E_CUDA: return "CUDA error (router poisoned)";
+    case ARGUS_E_NCCL: return "NCCL error (router poisoned)";
+    case ARGUS_E_STATE: return "router poisoned or call invalid in this mode";
+    case ARGUS_E_UNIMPLEMENTED: return "not implemented";
+    default: return "unknown argus code";
+  }
+}
+
+int argus_nccl_unique_id(void* out128) {
+  if (!out128) return ARGUS_E_INVALID;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (!nccl().ok || nccl().GetUniqueId(&id) != ncclSuccess) return ARGUS_E_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return ARGUS_OK;
+}
+
+int argus_quota_from_fractions(const double* f, int32_t L, int32_t N, int32_t* c_out) {
+  if (!f || !c_out || L <= 0 || L > 64 || N < 0) return ARGUS_E_INVALID;
+  double S = 0.0;
+  for (int32_t v = 0; v < L; ++v) {
+    if (!(f[v] >= 0.0) || !std::isfinite(f[v])) return ARGUS_E_INVALID;
+    S += f[v];
+  }
+  if (!(S > 0.0)) return ARGUS_E_INVALID;
+  double fr[64];
+  int64_t used = 0;
+  for (int32_t v = 0; v < L; ++v) {
+    const double t = (f[v] * (double)N) / S;
+    const double fl = std::floor(t);
+    c_out[v] = (int32_t)fl;
+    fr[v] = t - fl;
+    used += c_out[v];
+  }
+  int64_t left = (int64_t)N - used;
+  while (left > 0) {  // one leftover unit each to the largest fractional parts, ties -> lower v
+    int32_t best = -1;
+    for (int32_t v = 0; v < L; ++v)
+      if (fr[v] >= 0.0 && (best < 0 || fr[v] > fr[best])) best = v;
+    c_out[best] += 1;
+    fr[best] = -1.0;
+    --left;
+  }
+  while (left < 0) {  // rounding guard: remove from the smallest parts, ties -> higher v
+    int32_t worst = -1;
+    for (int32_t v = L - 1; v >= 0; --v)
+      if (c_out[v] > 0 && (worst < 0 || fr[v] < fr[worst])) worst = v;
+    c_out[worst] -= 1;
+    fr[worst] = 2.0;
+    ++left;
+  }
+  return ARGUS_OK;
+}
+
+int argus_route_destroy(argus_router* r) {
+  if (!r) return ARGUS_E_INVALID;
+  cudaSetDevice(r->cfg.device);
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xT,  r->d_W1sT,     r->d_b1,
+                  r->d_W2T,   r->d_b2,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
+                  r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
+                  r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
+                  r->d_order, r->d_flags};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (r->h_flags) cudaFreeHost(r->h_flags);
+  for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
+  for (auto e : r->ev_pool) cudaEventDestroy(e);
+  if (r->comm) nccl().CommDestroy(r->comm);
+  if (r->own_stream && r->stream) cudaStreamDestroy(r->stream);
+  delete r;
+  return ARGUS_OK;
+}
+
+int argus_route_init(const argus_config* cfg, const argus_option* opts, const float* w1,
+                     const float* b1, const float* w2, const float* b2, argus_router** out) {
+  if (!cfg || !out) return ARGUS_E_INVALID;
+  *out = nullptr;
+  const argus_config& c = *cfg;
+  if (c.d < 64 || c.d > 768 || c.d % 64 != 0) return ARGUS_E_INVALID;
+  if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
+  if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
+  if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
+  if (c.max_batch < 1 || c.max_batch > 8192) return ARGUS_E_INVALID;
+  if (c.capacity < 0 || c.capacity > 0xFFFFFFFELL) return ARGUS_E_INVALID;
+  if (!(c.delta > 0.f && c.delta <= 1.f)) return ARGUS_E_INVALID;
+  if (c.world < 1 || c.rank < 0 || c.rank >= c.world || c.device < 0) return ARGUS_E_INVALID;
+  const bool root_data = (c.world == 1 || c.rank == 0 || c.nccl_unique_id == nullptr);
+  if (root_data) {
+    if (!opts || !w1 || !b1 || !w2 || !b2) return ARGUS_E_INVALID;
+    if (opts[0].k_skip != 0) return ARGUS_E_INVALID;
+    for (int v = 0; v < c.L; ++v) {
+      if (opts[v].k_skip < 0 || opts[v].k_skip >= 50) return ARGUS_E_INVALID;
+      if (!std::isfinite(opts[v].p_th_qpm)) return ARGUS_E_INVALID;
+      if (v > 0 && opts[v].p_th_qpm < opts[v - 1].p_th_qpm) return ARGUS_E_INVALID;
+      if (std::isnan(opts[v].sim_gate)) return ARGUS_E_INVALID;
+    }
+    if (!finite_all(w1, (int64_t)c.hidden * (c.d + c.k)) || !finite_all(b1, c.hidden) ||
+        !finite_all(w2, (int64_t)c.L * c.hidden) || !finite_all(b2, c.L))
+      return ARGUS_E_INVALID;
+  }
+
+  argus_router* r = new (std::nothrow) argus_router();
+  if (!r) return ARGUS_E_CUDA;
+  r->cfg = c;
+  r->cfg.nccl_unique_id = nullptr;
+  int rc;
+#define TRY_RC(x)                   \
+  do {                              \
+    if ((rc = (x)) != ARGUS_OK) {   \
+      argus_route_destroy(r);       \
+      return rc;                    \
+    }                               \
+  } while (0)
+  if (cudaSetDevice(c.device) != cudaSuccess) { delete r; return ARGUS_E_CUDA; }
+  cudaDeviceGetAttribute(&r->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  if (c.stream) {
+    r->stream = (cudaStream_t)c.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) { delete r; return ARGUS_E_CUDA; }
+    r->own_stream = true;
+  }
+  if (c.world > 1 && c.nccl_unique_id) {
+    ncclUniqueId id;
+    memcpy(&id, c.nccl_unique_id, sizeof(id));
+    if (!nccl().ok || nccl().CommInitRank(&r->comm, c.world, id, c.rank) != ncclSuccess) {
+      r->comm = nullptr;
+      argus_route_destroy(r);
+      return ARGUS_E_NCCL;
+    }
+  }
+  const int d = c.d, k = c.k, L = c.L, H = c.hidden, G = c.world;
+  r->cap_local = (c.capacity + G - 1) / G;
+  r->n_pad_max = ((c.max_batch + 127) / 128) * 128;
+  r->p_max = 2 * r->num_sms;
+  const int64_t stage_rows = std::max<int64_t>(c.max_batch, INSERT_CHUNK);
+  TRY_RC(dalloc(r, &r->d_kskip, L));
+  TRY_RC(dalloc(r, &r->d_pth, L));
+  TRY_RC(dalloc(r, &r->d_gate, L));
+  TRY_RC(dalloc(r, &r->d_W1xT, (size_t)d * H));
+  TRY_RC(dalloc(r, &r->d_W1sT, (size_t)k * H));
+  TRY_RC(dalloc(r, &r->d_b1, H));
+  TRY_RC(dalloc(r, &r->d_W2T, (size_t)H * L));
+  TRY_RC(dalloc(r, &r->d_b2, L));
+  TRY_RC(dalloc(r, &r->d_Cb, (size_t)(r->cap_local + 256) * d));
+  TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
+  TRY_RC(dalloc(r, &r->d_Xstage, (size_t)stage_rows * d));
+  TRY_RC(dalloc(r, &r->d_Xb, (size_t)r->n_pad_max * d));
+  TRY_RC(dalloc(r, &r->d_invq, (size_t)r->n_pad_max));
+  TRY_RC(dalloc(r, &r->d_partial, (size_t)r->p_max * c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_idx, (size_t)c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_rhat, (size_t)c.max_batch * L));
+  TRY_RC(dalloc(r, &r->d_pref, (size_t)c.max_batch * L));
+  TRY_RC(dalloc(r, &r->d_ccount, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_cmask, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_status, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_option, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_order, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_flags, 1));
+  if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  // zero the cache tail so TMA / vector loads past M never see garbage
+  if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
+      cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
+      cudaMemsetAsync(r->d_flags, 0, sizeof(uint32_t), r->stream) != cudaSuccess) {
+    argus_route_destroy(r);
+    return ARGUS_E_CUDA;
+  }
+
+  // options + weights: staged through the fp32 staging buffer, transposed on device
+  std::vector<int32_t> ks(L);
+  std::vector<float> pth(L), gate(L);
+  if (root_data) {
+    for (int v = 0; v < L; ++v) {
+      ks[v] = opts[v].k_skip;
+      pth[v] = opts[v].p_th_qpm;
+      gate[v] = opts[v].k_skip == 0 ? -INFINITY : opts[v].sim_gate;
+    }
+  }
+  float* d_w1 = nullptr;
+  float* d_w2 = nullptr;
+  TRY_RC(dalloc(r, &d_w1, (size_t)H * (d + k)));
+  TRY_RC(dalloc(r, &d_w2, (size_t)L * H));
+  auto cleanup_tmp = [&]() { cudaFree(d_w1); cudaFree(d_w2); };
+  if (root_data) {
+    if (cudaMemcpy(r->d_kskip, ks.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(r->d_pth, pth.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(r->d_gate, gate.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_w1, w1, sizeof(float) * H * (d + k), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d_w2, w2, sizeof(float) * L * H, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(r->d_b1, b1, sizeof(float) * H, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(r->d_b2, b2, sizeof(float) * L, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cleanup_tmp();
+      argus_route_destroy(r);
+      return ARGUS_E_CUDA;
+    }
+  }
+  if (nccl_mode(r)) {  // C-4: rank 0's table and weights to every rank
+    nccl().GroupStart();
+    nccl().Broadcast(r->d_kskip, r->d_kskip, L, ncclInt32, 0, r->comm, r->stream);
+    nccl().Broadcast(r->d_pth, r->d_pth, L, ncclFloat32, 0, r->comm, r->stream);
+    nccl().Broadcast(r->d_gate, r->d_gate, L, ncclFloat32, 0, r->comm, r->stream);
+    nccl().Broadcast(d_w1, d_w1, (size_t)H * (d + k), ncclFloat32, 0, r->comm, r->stream);
+    nccl().Broadcast(d_w2, d_w2, (size_t)L * H, ncclFloat32, 0, r->comm, r->stream);
+    nccl().Broadcast(r->d_b1, r->d_b1, H, ncclFloat32, 0, r->comm, r->stream);
+    if (nccl().GroupEnd() != ncclSuccess ||
+        nccl().Broadcast(r->d_b2, r->d_b2, L, ncclFloat32, 0, r->comm, r->stream) != ncclSuccess) {
+      cleanup_tmp();
+      argus_route_destroy(r);
+      return ARGUS_E_NCCL;
+    }
+  }
+  {
+    const int64_t tot = (int64_t)H * (d + k) + (int64_t)L * H;
+    k_prep_weights<<<(unsigned)((tot + 255) / 256), 256, 0, r->stream>>>(d_w1, d_w2, d, k, H, L, r->d_W1xT,
+                                                                          r->d_W1sT, r->d_W2T);
+    r->launches++;
+  }
+  if (cudaStreamSynchronize(r->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+    cleanup_tmp();
+    argus_route_destroy(r);
+    return ARGUS_E_CUDA;
+  }
+  cleanup_tmp();
+#undef TRY_RC
+  *out = r;
+  return ARGUS_OK;
+}
+
+int argus_cache_size(const argus_router* r, int64_t* m_out) {
+  if (!r || !m_out) return ARGUS_E_INVALID;
+  *m_out = r->m_global;
+  return ARGUS_OK;
+}
+
+int argus_launch_count(const argus_router* r, int64_t* n_out) {
+  if (!r || !n_out) return ARGUS_E_INVALID;
+  *n_out = r->launches;
+  return ARGUS_OK;
+}
+
+int argus_get_stream(const argus_router* r, void** stream_out) {
+  if (!r || !stream_out) return ARGUS_E_INVALID;
+  *stream_out = (void*)r->stream;
+  return ARGUS_OK;
+}
+
+static int insert_impl(argus_router* r, const float* emb, int64_t n, int64_t* first_id, bool on_device) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (n < 0) return ARGUS_E_INVALID;
+  const bool root = r->cfg.rank == 0 || !nccl_mode(r);
+  if (root && n > 0 && !emb) return ARGUS_E_INVALID;
+  if (r->m_global + n > r->cfg.capacity) return ARGUS_E_CAPACITY;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  const int d = r->cfg.d;
+  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+  for (int64_t off = 0; off < n; off += INSERT_CHUNK) {
+    const int64_t m = std::min<int64_t>(INSERT_CHUNK, n - off);
+    const float* src = nullptr;
+    if (root) {
+      if (on_device && !nccl_mode(r)) {
+        src = emb + off * d;
+      } else {
+        CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, emb + off * d, sizeof(float) * m * d,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, r->stream));
+        src = r->d_Xstage;
+      }
+    } else {
+      src = r->d_Xstage;
+    }
+    if (nccl_mode(r))  // C-3: rank 0's rows to every rank; each keeps its stripe
+      NC_TRY(r, nccl().Broadcast(r->d_Xstage, r->d_Xstage, (size_t)m * d, ncclFloat32, 0, r->comm, r->stream));
+    {
+      StageScope sc(r, ARGUS_STAGE_INSERT);
+      launch_insert_rows(src, m, r->m_global + off, d, r->cfg.rank, r->cfg.world, r->d_Cb, r->d_invc,
+                         r->d_flags, r->stream);
+    }
+    LAUNCHED(r);
+  }
+  CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));
+  uint32_t fl = *r->h_flags;
+  if (nccl_mode(r)) {  // every rank must agree on validity (each saw only its stripe)
+    CU_TRY(r, cudaMemcpyAsync(r->d_flags, &fl, 4, cudaMemcpyHostToDevice, r->stream));
+    NC_TRY(r, nccl().AllReduce(r->d_flags, r->d_flags, 1, ncclUint32, ncclMax, r->comm, r->stream));
+    CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
+    CU_TRY(r, cudaStreamSynchronize(r->stream));
+    fl = *r->h_flags;
+  }
+  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+  if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;  // M unchanged: rows past M are ignored
+  if (first_id) *first_id = r->m_global;
+  r->m_global += n;
+  return ARGUS_OK;
+}
+
+int argus_cache_insert(argus_router* r, const float* emb, int64_t n, int64_t* first_id) {
+  return insert_impl(r, emb, n, first_id, false);
+}
+
+int argus_cache_insert_dev(argus_router* r, const float* emb_dev, int64_t n, int64_t* first_id) {
+  return insert_impl(r, emb_dev, n, first_id, true);
+}
+
+static int64_t local_rows(const argus_router* r) {
+  const int64_t G = r->cfg.world, rk = r->cfg.rank;
+  return (r->m_global + G - 1 - rk) / G;
+}
+
+int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (N < 1 || N > r->cfg.max_batch || !keys_dev) return ARGUS_E_INVALID;
+  const bool root = r->cfg.rank == 0 || !nccl_mode(r);
+  if (root && !prompts_dev) return ARGUS_E_INVALID;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  const int d = r->cfg.d, k = r->cfg.k;
+  const int n_pad = ((N + 127) / 128) * 128;
+  // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
+  if (root) {
+    StageScope sc(r, ARGUS_STAGE_PREP);
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_flags, r->stream);
+    LAUNCHED(r);
+  }
+  if (nccl_mode(r)) {
+    NC_TRY(r, nccl().GroupStart());
+    NC_TRY(r, nccl().Broadcast(r->d_Xb, r->d_Xb, (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
+    NC_TRY(r, nccl().Broadcast(r->d_invq, r->d_invq, (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
+    NC_TRY(r, nccl().GroupEnd());
+  }
+  ScanArgs a{};
+  a.Xb = r->d_Xb;
+  a.inv_q = r->d_invq;
+  a.Cb = r->d_Cb;
+  a.inv_c = r->d_invc;
+  a.m_local = local_rows(r);
+  a.N = N;
+  a.n_pad = n_pad;
+  a.d = d;
+  a.k = k;
+  a.rank = r->cfg.rank;
+  a.world = r->cfg.world;
+  a.partial = r->d_partial;
+  a.P = std::min(scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
+  a.tmap_c = nullptr;
+  {
+    StageScope sc(r, ARGUS_STAGE_SCAN);
+    launch_scan(a, r->stream);
+  }
+  LAUNCHED(r);
+  {
+    StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
+    launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
+  }
+  LAUNCHED(r);
+  return ARGUS_OK;
+}
+
+int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
+                           const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
+                           float* topk_score_dev, float* quality_dev, uint8_t* status_dev) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (N < 1 || N > r->cfg.max_batch || G < 1 || !keys_all_dev || !quota) return ARGUS_E_INVALID;
+  const int L = r->cfg.L, k = r->cfg.k;
+  QuotaArg q{};
+  for (int v = 0; v < L; ++v) {
+    if (quota[v] < 0) return ARGUS_E_INVALID;
+    q.c[v] = quota[v];
+  }
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  float* score = topk_score_dev ? topk_score_dev : r->d_score;
+  uint32_t* idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
+  {
+    StageScope sc(r, ARGUS_STAGE_MERGE_GLOBAL);
+    launch_merge_topk(keys_all_dev, G, N, k, r->d_keys, idx, score, r->stream);
+  }
+  LAUNCHED(r);
+  MlpArgs m{};
+  m.Xb = r->d_Xb;
+  m.topk_score = score;
+  m.W1xT = r->d_W1xT;
+  m.W1sT = r->d_W1sT;
+  m.b1 = r->d_b1;
+  m.W2T = r->d_W2T;
+  m.b2 = r->d_b2;
+  m.kskip = r->d_kskip;
+  m.pth = r->d_pth;
+  m.gate = r->d_gate;
+  m.delta = r->cfg.delta;
+  m.N = N;
+  m.d = r->cfg.d;
+  m.k = k;
+  m.H = r->cfg.hidden;
+  m.L = L;
+  m.rhat = quality_dev ? quality_dev : r->d_rhat;
+  m.pref = r->d_pref;
+  m.ccount = r->d_ccount;
+  m.cmask = r->d_cmask;
+  uint8_t* status = status_dev ? status_dev : r->d_status;
+  m.status = status;
+  {
+    StageScope sc(r, ARGUS_STAGE_MLP);
+    launch_mlp(m, r->stream);
+  }
+  LAUNCHED(r);
+  AssignArgs as{};
+  as.pref = r->d_pref;
+  as.ccount = r->d_ccount;
+  as.cmask = r->d_cmask;
+  // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
+  for (int v = 0; v < 32; ++v) as.quota[v] = v < L ? q.c[v] : 0;
+  as.N = N;
+  as.L = L;
+  as.order = r->d_order;
+  as.option_out = option_out_dev ? option_out_dev : r->d_option;
+  as.status = status;
+  as.flags = r->d_flags;
+  {
+    StageScope sc(r, ARGUS_STAGE_ASSIGN);
+    launch_assign(as, r->stream);
+  }
+  LAUNCHED(r);
+  return ARGUS_OK;
+}
+
+int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, const int32_t* quota,
+                          int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
+                          float* quality_dev, uint8_t* status_dev) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;  // external mode: use partial/finish
+  if (N < 1 || N > r->cfg.max_batch || !quota || !option_out_dev || !topk_idx_dev || !topk_score_dev)
+    return ARGUS_E_INVALID;
+  for (int v = 0; v < r->cfg.L; ++v)
+    if (quota[v] < 0) return ARGUS_E_INVALID;
+  rc = argus_route_partial_dev(r, prompts_dev, N, r->d_keys);
+  if (rc) return rc;
+  const uint64_t* all = r->d_keys;
+  int G = 1;
+  if (nccl_mode(r)) {  // C-2: N*k candidate keys from every shard
+    NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
+    all = r->d_keys_all;
+    G = r->cfg.world;
+  }
+  return argus_route_finish_dev(r, all, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
+                                quality_dev, status_dev);
+}
+
+int argus_sync(argus_router* r) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));
+  const uint32_t fl = *r->h_flags;
+  if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
+  if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
+  return ARGUS_OK;
+}
+
+int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                      int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
+                      uint8_t* status_out) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  const bool root = r->cfg.rank == 0 || !nccl_mode(r);
+  if (N < 1 || N > r->cfg.max_batch || !quota || !option_out || !topk_idx || !topk_score) return ARGUS_E_INVALID;
+  if (root && !prompts) return ARGUS_E_INVALID;
+  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
+  rc = argus_sync(r);  // drain earlier async work and clear its deferred flags
+  if (rc < 0) return rc;
+  if (root)
+    CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, prompts, sizeof(float) * N * d, cudaMemcpyHostToDevice, r->stream));
+  rc = argus_route_batch_dev(r, r->d_Xstage, N, quota, r->d_option, r->d_idx, r->d_score, r->d_rhat,
+                             r->d_status);
+  if (rc) return rc;
+  CU_TRY(r, cudaMemcpyAsync(option_out, r->d_option, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaMemcpyAsync(topk_idx, r->d_idx, sizeof(uint32_t) * N * k, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaMemcpyAsync(topk_score, r->d_score, sizeof(float) * N * k, cudaMemcpyDeviceToHost, r->stream));
+  if (quality_out)
+    CU_TRY(r, cudaMemcpyAsync(quality_out, r->d_rhat, sizeof(float) * N * L, cudaMemcpyDeviceToHost, r->stream));
+  if (status_out)
+    CU_TRY(r, cudaMemcpyAsync(status_out, r->d_status, N, cudaMemcpyDeviceToHost, r->stream));
+  return argus_sync(r);
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// kernels.h -- internal launchers of libargus (not part of the C ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace argus {
+
+// error flags written by kernels into a device word (bitwise OR)
+enum : uint32_t { FLAG_INVALID_INPUT = 1u, FLAG_OVERFLOW = 2u };
+
+struct ScanArgs {
+  const __nv_bfloat16* Xb;   // [n_pad][d] bf16 prompts (rows >= N are zero)
+  const float* inv_q;        // [n_pad]
+  const __nv_bfloat16* Cb;   // [cap_local][d] bf16 cache shard
+  const float* inv_c;        // [cap_local]
+  int64_t m_local;           // rows valid in this shard
+  int32_t N, n_pad, d, k;
+  int32_t rank, world;       // global id g = slot * world + rank
+  uint64_t* partial;         // [P][N][k] per-CTA-range candidates
+  int32_t P;                 // number of cache ranges (filled by the planner)
+  const void* tmap_c;        // CUtensorMap* (device-visible, __grid_constant__ copy) for Cb
+};
+
+// K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
+// g % world == rank go to slot g / world.
+void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank,
+                        int32_t world, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags,
+                        cudaStream_t s);
+
+// K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
+void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
+                         float* inv_q, uint32_t* flags, cudaStream_t s);
+
+// K1+K2: fused scan + per-range top-k -> partial [P][N][k].  Returns P used.
+int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);
+void launch_scan(const ScanArgs& a, cudaStream_t s);
+
+// K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
+// decoding ids / scores.
+void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint64_t* keys_out,
+                       uint32_t* idx_out, float* score_out, cudaStream_t s);
+
+struct MlpArgs {
+  const __nv_bfloat16* Xb;   // [n_pad][d]
+  const float* topk_score;   // [N][k]
+  const __nv_bfloat16* W1xT; // [d][H]
+  const float* W1sT;         // [k][H]
+  const float* b1;           // [H]
+  const float* W2T;          // [H][L]
+  const float* b2;           // [L]
+  const int32_t* kskip;      // [L]
+  const float* pth;          // [L]
+  const float* gate;         // [L]
+  float delta;
+  int32_t N, d, k, H, L;
+  float* rhat;               // [N][L]
+  uint8_t* pref;             // [N][L] (0xFF past |A_i|)
+  uint8_t* ccount;           // [N] |C_i|
+  uint32_t* cmask;           // [N] compliance mask
+  uint8_t* status;           // [N] base status bits (GATED_ALL)
+};
+// K3 + A5: predictor MLP with fused compliance / preference / priority keys.
+void launch_mlp(const MlpArgs& a, cudaStream_t s);
+
+struct AssignArgs {
+  const uint8_t* pref;
+  const uint8_t* ccount;
+  const uint32_t* cmask;
+  int32_t quota[32];         // [L] per-option quotas c_v (by value)
+  int32_t N, L;
+  int32_t* order;            // [N] scratch: priority order
+  int32_t* option_out;       // [N]
+  uint8_t* status;           // [N] in: base bits, out: + OVERFLOW / NONCOMPLIANT
+  uint32_t* flags;
+};
+// K4: priority counting sort + serial dictatorship.
+void launch_assign(const AssignArgs& a, cudaStream_t s);
+
+}  // namespace argus

@@ -1,0 +1,149 @@
+"""Parity helpers: compare the CUDA path with the oracle.
+
+Test infrastructure (imports oracle/).  Tolerances come from BASELINE.json
+north_star: "similarity and predictor outputs within 2e-2 absolute (bf16 inputs,
+fp32 accumulate); top-k index sets and final assignments bit-exact, except where
+the oracle's score gap at the boundary is below 1e-3".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+SCORE_TOL = 2e-2    # T1, M1, M2
+GAP_TOL = 1e-3      # T3 boundary-gap exemption, A2 fragility
+DELTA32 = float(np.float32(oracle.DELTA))
+
+
+def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
+    """T1 + T3.  Returns dict(exempt_rows, max_score_err).  Raises AssertionError.
+
+    For each row the oracle's top-(k+1) fixes tie groups (maximal runs of
+    consecutive oracle scores closer than GAP_TOL).  Entries whose group is fully
+    inside the top-k must appear (as a set per group, in group order); the group
+    straddling position k may be filled by any of its members.  Every returned id
+    must score (in the oracle) >= s_(k) - GAP_TOL, and |gpu - oracle| <= SCORE_TOL
+    for every returned (id, score)."""
+    rows = range(X.shape[0]) if rows is None else rows
+    Xs = X[list(rows)]
+    M = cache.shape[0]
+    kk = min(k + 1, max(M, 1))
+    osc, oix = oracle.scan_topk(Xs, cache, kk)
+    exempt, max_err = 0, 0.0
+    for r, i in enumerate(rows):
+        gi = [int(x) for x in gpu_idx[i]]
+        gs = [float(x) for x in gpu_score[i]]
+        nreal = min(k, M)
+        # padding
+        assert gi[nreal:] == [0xFFFFFFFF] * (k - nreal), (i, gi)
+        assert all(s == -1.0 for s in gs[nreal:]), (i, gs)
+        if nreal == 0:
+            continue
+        o_s = osc[r]
+        o_i = [int(x) for x in oix[r]]
+        # scores of the GPU's ids, in the oracle
+        g_true = np.array([oracle.cosine(X[i], cache[g]) for g in gi[:nreal]])
+        err = np.abs(g_true - np.array(gs[:nreal]))
+        max_err = max(max_err, float(err.max()))
+        assert err.max() <= SCORE_TOL, (i, err.max())
+        # tie groups over the oracle's k(+1) list
+        groups, cur = [], [0]
+        for t in range(1, len(o_i)):
+            if o_s[t - 1] - o_s[t] < GAP_TOL:
+                cur.append(t)
+            else:
+                groups.append(cur)
+                cur = [t]
+        groups.append(cur)
+        kth = o_s[nreal - 1]
+        boundary_tie = len(o_i) > nreal and (o_s[nreal - 1] - o_s[nreal] < GAP_TOL)
+        if boundary_tie:
+            exempt += 1
+        pos = 0
+        for grp in groups:
+            if pos >= nreal:
+                break
+            members = [o_i[t] for t in grp if t < len(o_i)]
+            take = min(len(members), nreal - pos)
+            got = gi[pos:pos + take]
+            if take == len(members) and not (boundary_tie and grp[-1] >= nreal - 1):
+                assert sorted(got) == sorted(members), (i, got, members, o_s)
+            else:   # the straddling group: any members with score >= s_k - GAP_TOL
+                for g, sg in zip(got, g_true[pos:pos + take]):
+                    assert sg >= kth - GAP_TOL - 1e-12, (i, g, sg, kth)
+            pos += take
+        # order: GPU list sorted by its own scores, descending (ties -> lower id)
+        for t in range(nreal - 1):
+            assert (gs[t] > gs[t + 1]) or (gs[t] == gs[t + 1] and gi[t] < gi[t + 1]), (i, gs, gi)
+    return dict(exempt_rows=exempt, max_score_err=max_err, rows=len(list(rows)))
+
+
+def check_replay(gpu, opts, quota, delta=oracle.DELTA):
+    """A1: O6..O10 in fp64 on the GPU's own fp32 r and s_1 -> bit-exact options/status."""
+    rhat = gpu["quality"].astype(np.float64)
+    s1 = gpu["topk_score"][:, 0].astype(np.float64)
+    rep = oracle.assign(rhat, s1, opts, quota, delta)
+    np.testing.assert_array_equal(gpu["option"], rep["option"])
+    np.testing.assert_array_equal(gpu["status"], rep["status"])
+    return rep
+
+
+def check_mlp_replay(X, gpu, W1, b1, W2, b2):
+    """M1: oracle O5 on the GPU's top-k scores vs the GPU's r (<= 2e-2)."""
+    r = oracle.mlp(X, gpu["topk_score"].astype(np.float64), W1, b1, W2, b2)
+    err = float(np.abs(r - gpu["quality"]).max())
+    assert err <= SCORE_TOL, err
+    return err
+
+
+def invariants(gpu, opts, quota, delta=oracle.DELTA):
+    """A3: I1 (quotas), I2 (no below-threshold option while a compliant one is
+    free), I3 (full model compliant), I6 (everyone assigned)."""
+    a, st, rq = gpu["option"], gpu["status"], gpu["quality"]
+    L = len(opts)
+    ok = (st & oracle.OVERFLOW) == 0
+    cnt = np.bincount(a[ok], minlength=L)
+    assert np.all(cnt <= quota), (cnt, quota)
+    rem = np.asarray(quota) - cnt
+    s1 = gpu["topk_score"][:, 0]
+    for i in range(a.size):
+        assert rq[i, 0] == 1.0
+        if ok[i] and rq[i, a[i]] < np.float32(delta):
+            for v in range(L):
+                adm = v == 0 or opts[v]["k_skip"] == 0 or s1[i] >= np.float32(opts[v]["sim_gate"])
+                if adm and rq[i, v] >= np.float32(delta):
+                    assert rem[v] == 0, (i, v)
+    assert a.size == rq.shape[0]
+
+
+def end_to_end_prefix(ores, gpu, opts, quota):
+    """A2: walk prompts in the oracle's priority order; assignments must match
+    exactly until the first prompt whose decision is fragile (within GAP_TOL of a
+    threshold, a gate, or a competing free option), or that a fragile prompt could
+    precede on the GPU.  Returns the matched fraction."""
+    r, s1 = ores["rhat"], ores["topk_score"][:, 0]
+    N, L = r.shape
+    gates = [(opts[v]["k_skip"] != 0, float(np.float32(opts[v]["sim_gate"]))) for v in range(L)]
+    ccount = np.array([bin(int(m)).count("1") for m in ores["cmp"]])
+    bucket_lo = {}
+    for i in range(N):
+        nd = sum(1 for v in range(1, L) if abs(r[i, v] - DELTA32) < GAP_TOL)
+        ng = sum(1 for v in range(L) if gates[v][0] and abs(s1[i] - gates[v][1]) < GAP_TOL)
+        if nd + ng:
+            bucket_lo[i] = ccount[i] - (nd + ng)
+    B = min(bucket_lo.values()) if bucket_lo else 10 ** 9
+    rem = np.array(quota, np.int64).copy()
+    matched = 0
+    for i in ores["order"]:
+        if ccount[i] >= B or i in bucket_lo:
+            break
+        a = int(ores["option"][i])
+        free = [v for v in range(L) if ores["adm"][i] >> v & 1 and rem[v] > 0 and v != a]
+        if any(abs(r[i, a] - r[i, v]) < GAP_TOL for v in free):
+            break
+        assert int(gpu["option"][i]) == a, (i, int(gpu["option"][i]), a)
+        if not (ores["status"][i] & oracle.OVERFLOW):
+            rem[a] -= 1
+        matched += 1
+    return matched / max(N, 1)

@@ -114,6 +114,8 @@ struct argus_router {
   int32_t* d_order = nullptr;      // [max_batch]
   uint32_t* d_flags = nullptr;     // error / overflow flags
   uint32_t* h_flags = nullptr;     // pinned mirror
+  CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
+  bool scan_simt = false;          // debug cross-check path (ARGUS_SCAN_SIMT=1)
   // stage profiling (argus_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -176,6 +178,30 @@ __global__ void k_prep_weights(const float* __restrict__ w1, const float* __rest
     const int v = (int)(t / H), j = (int)(t % H);
     W2T[(int64_t)j * L + v] = w2[t];
   }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// TMA descriptor of the cache shard: bf16 [rows][d] row-major, box 64 (K) x 64 (rows),
+// 128-byte swizzle (matches the UMMA K-major SW128 shared-memory descriptor).
+static bool make_cache_tmap(CUtensorMap* m, void* base, int64_t rows, int d) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static int finite_all(const float* p, int64_t n) {
@@ -343,7 +369,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (!cfg || !out) return ARGUS_E_INVALID;
   *out = nullptr;
   const argus_config& c = *cfg;
-  if (c.d < 64 || c.d > 768 || c.d % 64 != 0) return ARGUS_E_INVALID;
+  if (c.d < 64 || c.d % 64 != 0 || !scan_supported(c.d)) return ARGUS_E_INVALID;
   if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
   if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
   if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
@@ -427,6 +453,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_order, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_flags, 1));
   if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  if (!make_cache_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d)) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  r->scan_simt = getenv("ARGUS_SCAN_SIMT") != nullptr;
   // zero the cache tail so TMA / vector loads past M never see garbage
   if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
@@ -610,11 +638,12 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
   a.rank = r->cfg.rank;
   a.world = r->cfg.world;
   a.partial = r->d_partial;
-  a.P = std::min(scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
-  a.tmap_c = nullptr;
+  a.P = std::min(r->scan_simt ? scan_plan_ranges_simt(a.m_local, N, r->num_sms)
+                              : scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
   {
     StageScope sc(r, ARGUS_STAGE_SCAN);
-    launch_scan(a, r->stream);
+    if (r->scan_simt) launch_scan_simt(a, r->stream);
+    else launch_scan(a, &r->tmap_c, r->stream);
   }
   LAUNCHED(r);
   {

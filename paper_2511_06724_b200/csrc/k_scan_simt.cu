@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) k_scan_simt(ScanArgs a, int rang
   }
 }
 
-int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
+int scan_plan_ranges_simt(int64_t m_local, int32_t N, int num_sms) {
   const int nb = (N + SIMT_PB - 1) / SIMT_PB;
   int ranges = (4 * num_sms + nb - 1) / nb;
   if (ranges > SIMT_MAX_RANGES) ranges = SIMT_MAX_RANGES;
@@ -95,7 +95,7 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
   return ranges * SIMT_WARPS;
 }
 
-void launch_scan(const ScanArgs& a, cudaStream_t s) {
+void launch_scan_simt(const ScanArgs& a, cudaStream_t s) {
   const int ranges = a.P / SIMT_WARPS;
   const int64_t rows_per_range = (a.m_local + ranges - 1) / ranges;
   dim3 grid(ranges, (a.N + SIMT_PB - 1) / SIMT_PB);

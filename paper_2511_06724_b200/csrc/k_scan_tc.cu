@@ -1,0 +1,252 @@
+// k_scan_tc.cu -- K1+K2: the cosine cache scan with the fused per-prompt top-k
+// (SURVEY §8(a) rows A2 + A3; §2.1 "Using similarity search, the most
+// similar cached prompt is retrieved", §4.5, §4.7).
+//
+//   S[i, j] = (<Xb_i, Cb_j> * inv_c[j]) * inv_q[i]   bf16 x bf16 -> fp32 accumulate
+//   top-k per prompt i over (S desc, global id asc); S never reaches HBM.
+//
+// B200 design (DESIGN.md §"K1"):
+//   * one CTA per SM (persistent); CTA = one 128-prompt slice x one contiguous
+//     range of cache tiles; all CTAs of a range run concurrently, so the cache
+//     streams from HBM once and slices > 1 re-hit it in L2;
+//   * the prompt slice is the UMMA A operand and lives in TMEM for the whole
+//     kernel (128 lanes x d/2 columns, loaded once with tcgen05.st);
+//   * cache tiles of 64 rows are the B operand: TMA (128-byte swizzle) streams
+//     64x64 bf16 boxes through a STAGES-deep mbarrier ring in shared memory;
+//   * tcgen05.mma.cta_group::1.kind::f16, M=128 (prompts) x N=64 (cache rows) x
+//     K=16, issued by one thread into one of two TMEM accumulators
+//     (double-buffered, so the epilogue of tile t overlaps the MMAs of t+1);
+//   * epilogue: 4 warps, TMEM lane = prompt, so each thread owns ONE prompt and
+//     keeps its top-k in registers behind a float threshold: per score two
+//     FMULs, one compare; inserts are rare (~k ln(M/k) per prompt).
+// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 3 = idle,
+// 4..7 = Q loader + epilogue.
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace argus {
+
+namespace {
+constexpr int TN = 64;                   // cache rows per tile (UMMA N)
+constexpr int TM = 128;                  // prompts per CTA (UMMA M)
+constexpr int KBLK = 64;                 // bf16 per 128-byte swizzle row
+constexpr int STAGE_BYTES = TN * KBLK * 2;  // 8 KB
+constexpr int STAGES = 24;
+constexpr int THREADS = 256;
+constexpr int ACC_COL0 = 384;            // accumulators after the resident Q (d <= 768)
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/;
+}  // namespace
+
+struct ScanSmem {  // placed after the stage ring
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint64_t qready;
+  uint32_t tmem_base;
+};
+
+// Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
+// prompt: s = (acc * inv_c) * inv_q, threshold compare, rare register insert.
+template <int KMAX>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const float4* __restrict__ icp, float iq, int c0,
+                                          int cmax, uint32_t g0, uint32_t world, TopList<KMAX>& tl, float& thr) {
+#pragma unroll
+  for (int c4 = 0; c4 < 8; ++c4) {
+    const float4 ic = __ldg(icp + c4);
+#define ARGUS_EPI(E, ICV)                                                                  \
+    {                                                                                      \
+      const int c = c0 + c4 * 4 + (E);                                                     \
+      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v[c4 * 4 + (E)]), (ICV)), iq);   \
+      if (s >= thr && c < cmax) {                                                          \
+        tl.insert(pack_key(s, g0 + (uint32_t)c * world));                                  \
+        if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);                          \
+      }                                                                                    \
+    }
+    ARGUS_EPI(0, ic.x)
+    ARGUS_EPI(1, ic.y)
+    ARGUS_EPI(2, ic.z)
+    ARGUS_EPI(3, ic.w)
+#undef ARGUS_EPI
+  }
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, ScanArgs a, int slices, int ranges, int64_t n_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slice = blockIdx.x % slices;
+  const int range = blockIdx.x / slices;
+  const int64_t t_begin = n_tiles * range / ranges;
+  const int64_t t_end = n_tiles * (range + 1) / ranges;
+  const int KB = a.d / KBLK;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmap_c);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(tc::smem_u32(&sm->full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->empty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(tc::smem_u32(&sm->tfull[s]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->tempty[s]), 128);
+    }
+    tc::mbar_init(tc::smem_u32(&sm->qready), 128);
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) {
+    tc::tmem_alloc(tc::smem_u32(&sm->tmem_base), TMEM_COLS);
+    tc::tmem_relinquish();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ======================= TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = t_begin; t < t_end; ++t) {
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait(tc::smem_u32(&sm->empty[stage]), phase ^ 1);
+          const uint32_t fb = tc::smem_u32(&sm->full[stage]);
+          tc::mbar_arrive_expect_tx(fb, STAGE_BYTES);
+          tc::tma_load_2d(tc::smem_u32(ring + (size_t)stage * STAGE_BYTES), &tmap_c, fb, kb * KBLK,
+                          (int32_t)(t * TN));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
+      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
+      tc::fence_after();
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t local = 0;
+      for (int64_t t = t_begin; t < t_end; ++t, ++local) {
+        const int acc = (int)(local & 1);
+        const uint32_t aphase = (uint32_t)((local >> 1) & 1);
+        tc::mbar_wait(tc::smem_u32(&sm->tempty[acc]), aphase ^ 1);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem + ACC_COL0 + acc * TN;
+        for (int kb = 0; kb < KB; ++kb) {
+          tc::mbar_wait(tc::smem_u32(&sm->full[stage]), phase);
+          tc::fence_after();
+          const uint32_t sb = tc::smem_u32(ring + (size_t)stage * STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < KBLK / 16; ++kk) {
+            const uint32_t a_tmem = tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8);
+            tc::mma_ts(d_tmem, a_tmem, tc::desc_kmajor_sw128(sb + kk * 32), IDESC, (kb | kk) != 0);
+          }
+          tc::mma_commit(tc::smem_u32(&sm->empty[stage]));  // frees the smem slot when these MMAs finish
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit(tc::smem_u32(&sm->tfull[acc]));      // accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ======================= Q load into TMEM (A operand), then the epilogue
+    const int q = warp - 4;                 // TMEM lane quarter
+    const int p_local = q * 32 + lane;      // prompt within the slice
+    const int p = slice * TM + p_local;     // prompt within the batch
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(a.Xb + (int64_t)p * a.d);  // rows >= N are zero
+      for (int c = 0; c < a.d / 64; ++c) {   // 64 bf16 = 32 TMEM columns per chunk
+        uint32_t r[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 u = src[c * 8 + v];
+          r[4 * v + 0] = u.x;
+          r[4 * v + 1] = u.y;
+          r[4 * v + 2] = u.z;
+          r[4 * v + 3] = u.w;
+        }
+        tc::tmem_st32(tmem + lane_base + (uint32_t)(c * 32), r);
+      }
+      tc::tmem_wait_st();
+      tc::fence_before();
+      tc::mbar_arrive(tc::smem_u32(&sm->qready));
+    }
+    const bool active = p < a.N;
+    const float iq = a.inv_q[p];
+    TopList<KMAX> tl;
+    tl.clear();
+    float thr = -INFINITY;
+    int64_t local = 0;
+    for (int64_t t = t_begin; t < t_end; ++t, ++local) {
+      __syncwarp();
+      const int acc = (int)(local & 1);
+      const uint32_t aphase = (uint32_t)((local >> 1) & 1);
+      const int64_t j0 = t * TN;
+      tc::mbar_wait(tc::smem_u32(&sm->tfull[acc]), aphase);
+      tc::fence_after();
+      uint32_t v0[32], v1[32];
+      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + acc * TN, v0);
+      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + acc * TN + 32, v1);
+      tc::tmem_wait_ld();
+      tc::fence_before();
+      tc::mbar_arrive(tc::smem_u32(&sm->tempty[acc]));   // accumulator may be overwritten now
+      if (!active) continue;
+      const float4* icp = reinterpret_cast<const float4*>(a.inv_c + j0);
+      const int64_t rem_rows = a.m_local - j0;
+      const int cmax = rem_rows < TN ? (int)rem_rows : TN;
+      const uint32_t g0 = (uint32_t)(j0 * a.world + a.rank);
+      epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr);
+      epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr);
+    }
+    if (active) {
+      uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
+#pragma unroll
+      for (int t2 = 0; t2 < KMAX; ++t2)
+        if (t2 < a.k) out[t2] = tl.v[t2];
+    }
+  }
+
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
+  const int slices = (N + TM - 1) / TM;
+  int ranges = num_sms / slices;
+  if (ranges < 1) ranges = 1;
+  const int64_t n_tiles = (m_local + TN - 1) / TN;
+  if (ranges > n_tiles) ranges = (int)(n_tiles > 0 ? n_tiles : 1);
+  return ranges;
+}
+
+bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / 2 <= ACC_COL0; }
+
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, cudaStream_t s) {
+  const int slices = (a.N + TM - 1) / TM;
+  const int ranges = a.P;
+  const int64_t n_tiles = (a.m_local + TN - 1) / TN;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scan_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(k_scan_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attr = true;
+  }
+  const dim3 grid(slices * ranges);
+  if (a.k <= 4)
+    k_scan_tc<4><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, a, slices, ranges, n_tiles);
+  else
+    k_scan_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, a, slices, ranges, n_tiles);
+}
+
+}  // namespace argus

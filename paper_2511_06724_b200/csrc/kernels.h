@@ -1,6 +1,7 @@
 // kernels.h -- internal launchers of libargus (not part of the C ABI).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
@@ -19,7 +20,6 @@ struct ScanArgs {
   int32_t rank, world;       // global id g = slot * world + rank
   uint64_t* partial;         // [P][N][k] per-CTA-range candidates
   int32_t P;                 // number of cache ranges (filled by the planner)
-  const void* tmap_c;        // CUtensorMap* (device-visible, __grid_constant__ copy) for Cb
 };
 
 // K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
@@ -32,9 +32,14 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
                          float* inv_q, uint32_t* flags, cudaStream_t s);
 
-// K1+K2: fused scan + per-range top-k -> partial [P][N][k].  Returns P used.
+// K1+K2: fused tcgen05 scan + per-range top-k -> partial [P][N][k].
+// scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
 int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);
-void launch_scan(const ScanArgs& a, cudaStream_t s);
+bool scan_supported(int d);
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, cudaStream_t s);
+// SIMT reference-quality scan (debug cross-check only, ARGUS_SCAN_SIMT=1)
+int scan_plan_ranges_simt(int64_t m_local, int32_t N, int num_sms);
+void launch_scan_simt(const ScanArgs& a, cudaStream_t s);
 
 // K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
 // decoding ids / scores.

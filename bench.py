@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--sweep", default="", help="comma list of fixed N: per-N stage times to stderr")
+    ap.add_argument("--fixed-n", type=int, default=0, help="diagnostics: every batch has this N")
     return ap.parse_args()
 
 
@@ -173,8 +175,8 @@ def main():
     L = len(opts)
     W1, b1, W2, b2 = gen.mlp_weights(d, k, cfg.hidden, L, stress=cfg.stress)
     fr = gen.load_fractions(L, cfg.frac_base)
-    sizes = batch_sizes(cfg)
-    max_batch = max(sizes)
+    sizes = batch_sizes(cfg) if not args.fixed_n else [args.fixed_n] * N_TRACE
+    max_batch = max(max(sizes), max([int(x) for x in args.sweep.split(",") if x] or [0]))
 
     uid = None
     if world > 1:
@@ -187,12 +189,10 @@ def main():
 
     # ---- cache: generated chunk by chunk, inserted through the ABI (rank 0 authoritative)
     cg = gen.CacheGen(cfg.M, d, cfg.seed)
-    keep_rows = rank == 0 and not args.no_cpu_baseline
-    cache_rows = np.empty((cfg.M, d), np.float32) if keep_rows else None
+    cache_rows = np.empty((cfg.M, d), np.float32)  # kept: query repeats and the CPU baseline read it
     t0 = time.perf_counter()
     for a, chunk in cg.chunks():
-        if cache_rows is not None:
-            cache_rows[a:a + chunk.shape[0]] = chunk
+        cache_rows[a:a + chunk.shape[0]] = chunk
         r.argus_cache_insert(chunk)  # rank 0's rows are authoritative (broadcast by the library)
     t_insert = time.perf_counter() - t0
 
@@ -276,6 +276,9 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
 
+    if args.sweep:
+        sweep(args, r, cg, cache_rows, cfg, fr, out, stream, argus)
+
     # ---- roofline of the dominant kernel (the scan)
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
     scan_ms, scan_n = prof["scan"]
@@ -346,6 +349,35 @@ def main():
     r.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def sweep(args, r, cg, cache_rows, cfg, fr, out, stream, argus):
+    """Diagnostics: per fixed N, stage times and scan HBM GB/s (stderr only)."""
+    import torch
+    hbm = load_peaks()[0]
+    for n in [int(x) for x in args.sweep.split(",") if x]:
+        n = min(n, r.max_batch)
+        X = torch.from_numpy(gen.queries(cg, n, cfg.seed, 10_000 + n, cache_rows=cache_rows)).cuda()
+        q = argus.argus_quota_from_fractions(fr, n)
+        for _ in range(3):
+            r.argus_route_batch_dev(X, q, out["option"], out["topk_idx"], out["topk_score"], out["quality"],
+                                    out["status"])
+        r.argus_sync()
+        r.argus_profile_read()
+        r.argus_profile_enable(True)
+        reps = 20
+        for _ in range(reps):
+            r.argus_route_batch_dev(X, q, out["option"], out["topk_idx"], out["topk_score"], out["quality"],
+                                    out["status"])
+        r.argus_sync()
+        prof = r.argus_profile_read()
+        r.argus_profile_enable(False)
+        scan_ms = prof["scan"][0] / reps
+        gbs = cfg.M * (2 * cfg.d + 4) / (scan_ms / 1e3) / 1e9
+        tfl = 2.0 * n * cfg.M * cfg.d / (scan_ms / 1e3) / 1e12
+        stages = " ".join(f"{k}={v[0] / reps * 1e3:.1f}us" for k, v in prof.items() if v[1])
+        print(f"[sweep] N={n:5d} scan={scan_ms * 1e3:8.1f}us  {gbs:7.1f} GB/s ({gbs / hbm:.3f} of HBM)  "
+              f"{tfl:7.1f} TFLOP/s  | {stages}", file=sys.stderr, flush=True)
 
 
 def gen_quota(fr, n):

@@ -88,7 +88,7 @@ struct argus_router {
   float* d_pth = nullptr;
   float* d_gate = nullptr;
   // weights (device)
-  __nv_bfloat16* d_W1xT = nullptr;
+  __nv_bfloat16* d_W1xF = nullptr;  // [H*d] bf16, mma fragment order
   float* d_W1sT = nullptr;
   float* d_b1 = nullptr;
   float* d_W2T = nullptr;
@@ -164,15 +164,12 @@ static bool nccl_mode(const argus_router* r) { return r->cfg.world > 1 && r->com
 
 // transpose / round the predictor weights on the device (init time)
 __global__ void k_prep_weights(const float* __restrict__ w1, const float* __restrict__ w2, int d, int k,
-                               int H, int L, __nv_bfloat16* __restrict__ W1xT, float* __restrict__ W1sT,
-                               float* __restrict__ W2T) {
+                               int H, int L, float* __restrict__ W1sT, float* __restrict__ W2T) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = (int64_t)H * (d + k);
   if (tid < n1) {
     const int j = (int)(tid / (d + k)), c = (int)(tid % (d + k));
-    const float w = w1[tid];
-    if (c < d) W1xT[(int64_t)c * H + j] = __float2bfloat16_rn(w);
-    else W1sT[(int64_t)(c - d) * H + j] = w;
+    if (c >= d) W1sT[(int64_t)(c - d) * H + j] = w1[tid];
   } else if (tid < n1 + (int64_t)L * H) {
     const int64_t t = tid - n1;
     const int v = (int)(t / H), j = (int)(t % H);
@@ -348,7 +345,7 @@ int argus_route_destroy(argus_router* r) {
   if (!r) return ARGUS_E_INVALID;
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xT,  r->d_W1sT,     r->d_b1,
+  void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xF,  r->d_W1sT,     r->d_b1,
                   r->d_W2T,   r->d_b2,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
@@ -373,6 +370,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
   if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
   if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
+  if (mlp_smem_bytes(c.d, c.k, c.hidden, c.L) > 227 * 1024) return ARGUS_E_INVALID;
   if (c.max_batch < 1 || c.max_batch > 8192) return ARGUS_E_INVALID;
   if (c.capacity < 0 || c.capacity > 0xFFFFFFFELL) return ARGUS_E_INVALID;
   if (!(c.delta > 0.f && c.delta <= 1.f)) return ARGUS_E_INVALID;
@@ -429,7 +427,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_kskip, L));
   TRY_RC(dalloc(r, &r->d_pth, L));
   TRY_RC(dalloc(r, &r->d_gate, L));
-  TRY_RC(dalloc(r, &r->d_W1xT, (size_t)d * H));
+  TRY_RC(dalloc(r, &r->d_W1xF, (size_t)d * H));
   TRY_RC(dalloc(r, &r->d_W1sT, (size_t)k * H));
   TRY_RC(dalloc(r, &r->d_b1, H));
   TRY_RC(dalloc(r, &r->d_W2T, (size_t)H * L));
@@ -508,9 +506,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   }
   {
     const int64_t tot = (int64_t)H * (d + k) + (int64_t)L * H;
-    k_prep_weights<<<(unsigned)((tot + 255) / 256), 256, 0, r->stream>>>(d_w1, d_w2, d, k, H, L, r->d_W1xT,
-                                                                          r->d_W1sT, r->d_W2T);
-    r->launches++;
+    k_prep_weights<<<(unsigned)((tot + 255) / 256), 256, 0, r->stream>>>(d_w1, d_w2, d, k, H, L, r->d_W1sT,
+                                                                          r->d_W2T);
+    launch_prep_w1_frag(d_w1, d, k, H, r->d_W1xF, r->stream);
+    r->launches += 2;
   }
   if (cudaStreamSynchronize(r->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
     cleanup_tmp();
@@ -677,7 +676,7 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
   MlpArgs m{};
   m.Xb = r->d_Xb;
   m.topk_score = score;
-  m.W1xT = r->d_W1xT;
+  m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;
   m.W2T = r->d_W2T;

@@ -7,23 +7,36 @@
 // still admits, with a fixed deterministic tie-break"):
 //   rem <- c;  for i in priority order: a_i <- first v in pi_i with rem_v > 0;
 //   rem_{a_i} -= 1;  none -> a_i = 0, OVERFLOW.
-// The walk is one warp: lane r holds pi_i[r], lane v holds rem_v, the
-// availability mask is a ballot, the choice is ffs(ballot).
+// The walk is one warp over shared memory: lane r holds pi_i[r], lane v holds
+// rem_v, availability is a ballot, the choice is ffs(ballot).  The whole block
+// stages each chunk of preference rows (in priority order) into shared memory
+// first, so the serial walk never waits on global memory.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace argus {
 
 constexpr int ASSIGN_THREADS = 1024;
-constexpr int NB = 33;  // |C_i| in [1, 32]
+constexpr int NB = 33;      // |C_i| in [1, 32]
+constexpr int CH = 1024;    // prompts per staged chunk
+
+size_t assign_smem_bytes(int max_batch, int L) {
+  const int Lw = (L + 3) / 4 * 4;
+  return sizeof(int32_t) * (size_t)max_batch + (size_t)CH * Lw + sizeof(uint32_t) * CH + CH;
+}
 
 __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
-  extern __shared__ int32_t order_s[];           // [N]
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int N = a.N, L = a.L;
+  const int Lw = (L + 3) / 4 * 4;
+  int32_t* order_s = reinterpret_cast<int32_t*>(smraw);                  // [N]
+  uint8_t* pref_s = smraw + sizeof(int32_t) * (size_t)N;                 // [CH][Lw]
+  uint32_t* cm_s = reinterpret_cast<uint32_t*>(pref_s + (size_t)CH * Lw); // [CH]
+  uint8_t* opt_s = reinterpret_cast<uint8_t*>(cm_s + CH);                 // [CH] (option | 0x80 overflow)
   __shared__ int32_t base[NB];
   __shared__ int32_t tot[NB];
   __shared__ int32_t wcnt[ASSIGN_THREADS / 32][NB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int N = a.N, L = a.L;
 
   // ---- stable counting sort of prompts by |C_i|
   if (tid < NB) base[tid] = 0;
@@ -52,53 +65,71 @@ __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
     __syncthreads();
     if (b >= 0) order_s[base[b] + wcnt[warp][b] + wrank] = i;
     __syncthreads();
-    if (tid < NB) base[tid] += tot[tid];  // advance bucket bases by this chunk's counts
+    if (tid < NB) base[tid] += tot[tid];
     __syncthreads();
   }
 
-  // ---- serial dictatorship, one warp
-  if (warp != 0) return;
-  int rem = lane < L ? a.quota[lane] : 0;
+  // ---- serial dictatorship over staged chunks
+  int rem = lane < L ? a.quota[lane] : 0;       // only warp 0 uses it
   uint32_t avail = __ballot_sync(0xffffffffu, rem > 0);
   bool any_overflow = false;
-  int nxt_i = N > 0 ? order_s[0] : 0;
-  uint32_t nxt_pv = (N > 0 && lane < L) ? a.pref[(int64_t)nxt_i * L + lane] : 0xFFu;
-  for (int t = 0; t < N; ++t) {
-    const int i = nxt_i;
-    const uint32_t pv = nxt_pv;
-    if (t + 1 < N) {  // prefetch the next prompt's preference row
-      nxt_i = order_s[t + 1];
-      nxt_pv = lane < L ? a.pref[(int64_t)nxt_i * L + lane] : 0xFFu;
+  for (int c0 = 0; c0 < N; c0 += CH) {
+    const int n = min(CH, N - c0);
+    // stage preference rows / compliance masks of this chunk, in priority order
+    for (int x = tid; x < n * (Lw / 4); x += ASSIGN_THREADS) {
+      const int t = x / (Lw / 4), w = x - t * (Lw / 4);
+      const int i = order_s[c0 + t];
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = w * 4 + e;
+        const uint32_t pv = r < L ? a.pref[(int64_t)i * L + r] : 0xFFu;
+        word |= pv << (8 * e);
+      }
+      reinterpret_cast<uint32_t*>(pref_s + (size_t)t * Lw)[w] = word;
     }
-    const bool ok = pv != 0xFFu && ((avail >> pv) & 1u);
-    const uint32_t b = __ballot_sync(0xffffffffu, ok);
-    int opt = 0;
-    bool ovf = (b == 0);
-    if (!ovf) {
-      opt = (int)__shfl_sync(0xffffffffu, pv, __ffs(b) - 1);
-      if (lane == opt) --rem;
-      avail = __ballot_sync(0xffffffffu, rem > 0);
+    for (int t = tid; t < n; t += ASSIGN_THREADS) cm_s[t] = a.cmask[order_s[c0 + t]];
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t nxt = lane < L ? pref_s[lane] : 0xFFu;
+      for (int t = 0; t < n; ++t) {
+        const uint32_t pv = nxt;
+        if (t + 1 < n) nxt = lane < L ? pref_s[(size_t)(t + 1) * Lw + lane] : 0xFFu;
+        const bool ok = pv != 0xFFu && ((avail >> pv) & 1u);
+        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        int opt = 0;
+        if (b != 0) {
+          opt = (int)__shfl_sync(0xffffffffu, pv, __ffs(b) - 1);
+          if (lane == opt) --rem;
+          avail = __ballot_sync(0xffffffffu, rem > 0);
+        } else {
+          any_overflow = true;
+        }
+        if (lane == 0) opt_s[t] = (uint8_t)(opt | (b == 0 ? 0x80 : 0));
+      }
     }
-    if (lane == 0) {
-      const uint32_t cm = a.cmask[i];
+    __syncthreads();
+    for (int t = tid; t < n; t += ASSIGN_THREADS) {
+      const int i = order_s[c0 + t];
+      const int o = opt_s[t] & 0x7F;
       uint8_t st = a.status[i];
-      if (ovf) st |= 1u;                      // ARGUS_ST_OVERFLOW
-      if (!((cm >> opt) & 1u)) st |= 2u;      // ARGUS_ST_NONCOMPLIANT
+      if (opt_s[t] & 0x80) st |= 1u;                  // ARGUS_ST_OVERFLOW
+      if (!((cm_s[t] >> o) & 1u)) st |= 2u;           // ARGUS_ST_NONCOMPLIANT
       a.status[i] = st;
-      a.option_out[i] = opt;
+      a.option_out[i] = o;
     }
-    any_overflow |= ovf;
+    __syncthreads();
   }
-  if (lane == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
+  if (tid == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
 }
 
 void launch_assign(const AssignArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 4);
+    cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  k_assign<<<1, ASSIGN_THREADS, sizeof(int32_t) * (a.N > 0 ? a.N : 1), s>>>(a);
+  k_assign<<<1, ASSIGN_THREADS, assign_smem_bytes(a.N > 0 ? a.N : 1, a.L), s>>>(a);
 }
 
 }  // namespace argus

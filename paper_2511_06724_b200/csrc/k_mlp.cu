@@ -8,93 +8,121 @@
 //   C_i = {v in A_i : r_v >= delta}                     (reading R6)
 //   pi_i = A_i sorted by (r desc, p_th desc, v asc)     (reading R13)
 //
-// One CTA = H threads (one per hidden unit) x PB prompts.  W1x is stored
-// transposed [d][H] in bf16 so a warp's loads are coalesced; the prompt block
-// sits in shared memory as fp32.  Layer 2 + A5 run one warp per prompt with
-// lane v owning option v (L <= 32), so masks are ballots and the preference
-// rank is a 32-lane compare-count.
+// One CTA = 8 warps x 16 prompts.  Layer 1 is a [16 x d] x [d x H] bf16 product
+// on the tensor cores (mma.sync m16n8k16, fp32 accumulate; <0.03 % of the
+// scan's flops, so the legacy warp-level MMA is the right size here): the prompt
+// block sits in shared memory (padded rows, conflict-free fragment loads) and
+// W1x is pre-arranged at init in per-lane fragment order so each B fragment is
+// one coalesced 8-byte load.  Layer 2 + A5 run one warp per prompt with lane v
+// owning option v (L <= 32), so masks are ballots and the preference rank is a
+// 32-lane compare-count.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace argus {
 
-constexpr int PB = 8;  // prompts per CTA
+constexpr int PB = 16;  // prompts per CTA (the MMA M dimension)
+constexpr int MLP_THREADS = 256;
 
-__global__ void __launch_bounds__(1024) k_mlp(MlpArgs a) {
-  extern __shared__ float sm[];
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+__global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
   const int d = a.d, H = a.H, L = a.L, k = a.k;
-  float* xs = sm;                    // [d][PB]
-  float* ss = xs + (size_t)d * PB;   // [PB][k]
-  float* hs = ss + PB * k;           // [PB][H]
-  float* w2 = hs + (size_t)PB * H;   // [H][L]
+  const int RS = d + 8;                                              // padded bf16 row stride
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smraw);       // [PB][RS]
+  float* ss = reinterpret_cast<float*>(smraw + (size_t)PB * RS * 2);  // [PB][k]
+  float* hs = ss + PB * k;                                           // [PB][H + 4]
+  float* w2 = hs + (size_t)PB * (H + 4);                             // [H][L]
+  const int HS = H + 4;
   const int i0 = blockIdx.x * PB;
   const int nP = min(PB, a.N - i0);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int idx = tid; idx < d * PB; idx += blockDim.x) {
-    const int p = idx / d, l = idx - p * d;
-    xs[l * PB + p] = p < nP ? __bfloat162float(a.Xb[(int64_t)(i0 + p) * d + l]) : 0.f;
+  // prompt block (bf16) -> shared; rows past N are zero
+  for (int idx = tid; idx < PB * (d / 8); idx += MLP_THREADS) {
+    const int p = idx / (d / 8), c = idx - p * (d / 8);
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (p < nP) u = reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d)[c];
+    *reinterpret_cast<uint4*>(xs + p * RS + c * 8) = u;
   }
-  for (int idx = tid; idx < PB * k; idx += blockDim.x) {
+  for (int idx = tid; idx < PB * k; idx += MLP_THREADS) {
     const int p = idx / k;
     ss[idx] = p < nP ? a.topk_score[(int64_t)(i0 + p) * k + (idx - p * k)] : 0.f;
   }
-  for (int idx = tid; idx < H * L; idx += blockDim.x) w2[idx] = a.W2T[idx];
+  for (int idx = tid; idx < H * L; idx += MLP_THREADS) w2[idx] = a.W2T[idx];
   __syncthreads();
 
-  // ---- layer 1: thread j = hidden unit
-  for (int j = tid; j < H; j += blockDim.x) {
-    float acc[PB];
+  // ---- layer 1 on the tensor cores: warp -> 32 hidden units per pass
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
+  const int RSW = RS / 2;  // row stride in 32-bit words
+  const int KS = d / 16;
+  const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
+  for (int cc = warp; cc < H / 32; cc += MLP_THREADS / 32) {
+    float acc[4][4];
 #pragma unroll
-    for (int p = 0; p < PB; ++p) acc[p] = 0.f;
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
 #pragma unroll 4
-    for (int l = 0; l < d; ++l) {
-      const float w = __bfloat162float(a.W1xT[(int64_t)l * H + j]);
-      const float4 x0 = *reinterpret_cast<const float4*>(xs + l * PB);
-      const float4 x1 = *reinterpret_cast<const float4*>(xs + l * PB + 4);
-      acc[0] = __fmaf_rn(w, x0.x, acc[0]);
-      acc[1] = __fmaf_rn(w, x0.y, acc[1]);
-      acc[2] = __fmaf_rn(w, x0.z, acc[2]);
-      acc[3] = __fmaf_rn(w, x0.w, acc[3]);
-      acc[4] = __fmaf_rn(w, x1.x, acc[4]);
-      acc[5] = __fmaf_rn(w, x1.y, acc[5]);
-      acc[6] = __fmaf_rn(w, x1.z, acc[6]);
-      acc[7] = __fmaf_rn(w, x1.w, acc[7]);
-    }
-    for (int t = 0; t < k; ++t) {
-      const float w = a.W1sT[t * H + j];
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t af[4];
+      af[0] = x32[g * RSW + ks * 8 + t];
+      af[1] = x32[(g + 8) * RSW + ks * 8 + t];
+      af[2] = x32[g * RSW + ks * 8 + 4 + t];
+      af[3] = x32[(g + 8) * RSW + ks * 8 + 4 + t];
 #pragma unroll
-      for (int p = 0; p < PB; ++p) acc[p] = __fmaf_rn(w, ss[p * k + t], acc[p]);
+      for (int nt = 0; nt < 4; ++nt) {
+        const int nb = cc * 4 + nt;
+        const uint2 b = __ldg(wf + ((int64_t)nb * KS + ks) * 32 + lane);
+        mma_bf16_16816(acc[nt], af, b);
+      }
     }
-    const float bj = a.b1[j];
+    // epilogue: + W1s . s + b1, relu -> hs
 #pragma unroll
-    for (int p = 0; p < PB; ++p) hs[p * H + j] = fmaxf(__fadd_rn(acc[p], bj), 0.f);
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = g + (e >> 1) * 8;
+        const int j = (cc * 4 + nt) * 8 + 2 * t + (e & 1);
+        float z = acc[nt][e];
+        for (int q = 0; q < k; ++q) z = __fmaf_rn(a.W1sT[q * H + j], ss[row * k + q], z);
+        hs[row * HS + j] = fmaxf(__fadd_rn(z, a.b1[j]), 0.f);
+      }
+    }
   }
   __syncthreads();
 
   // ---- layer 2 + A5: warp per prompt, lane v = option v
-  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  for (int p = warp; p < nP; p += nwarps) {
+  for (int p = warp; p < nP; p += MLP_THREADS / 32) {
     const int i = i0 + p;
     const bool act = lane < L;
     float r = 0.f;
     if (act) {
       float z = a.b2[lane];
-      for (int j = 0; j < H; ++j) z = __fmaf_rn(w2[j * L + lane], hs[p * H + j], z);
+      const float* hp = hs + p * HS;
+#pragma unroll 8
+      for (int j = 0; j < H; ++j) z = __fmaf_rn(w2[j * L + lane], hp[j], z);
       r = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
       if (lane == 0) r = 1.0f;
     }
     const float s1 = ss[p * k];
-    const int ks = act ? a.kskip[lane] : 0;
+    const int ks_ = act ? a.kskip[lane] : 0;
     const float gate = act ? a.gate[lane] : 0.f;
-    const bool gated_pass = act && ks != 0 && s1 >= gate;
-    const bool adm = act && (lane == 0 || ks == 0 || s1 >= gate);
+    const bool gated_pass = act && ks_ != 0 && s1 >= gate;
+    const bool adm = act && (lane == 0 || ks_ == 0 || s1 >= gate);
     const bool cmp = adm && r >= a.delta;
     const uint32_t amask = __ballot_sync(0xffffffffu, adm);
     const uint32_t cmask = __ballot_sync(0xffffffffu, cmp);
-    const uint32_t gmask = __ballot_sync(0xffffffffu, act && ks != 0);
+    const uint32_t gmask = __ballot_sync(0xffffffffu, act && ks_ != 0);
     const uint32_t pmask = __ballot_sync(0xffffffffu, gated_pass);
-    // preference rank among admissible options
     const float pth = act ? a.pth[lane] : 0.f;
     int rank = 0;
     for (int u = 0; u < L; ++u) {
@@ -118,15 +146,41 @@ __global__ void __launch_bounds__(1024) k_mlp(MlpArgs a) {
   }
 }
 
+// W1x [H][d] (fp32 rows of w1 [H][d+k]) -> bf16 (RNE) in mma.sync B-fragment order:
+// Wf[(nb * KS + ks) * 32 + lane] = {W[n][k0..k0+1], W[n][k0+8..k0+9]},
+// n = nb * 8 + lane / 4, k0 = ks * 16 + (lane % 4) * 2.
+__global__ void k_prep_w1_frag(const float* __restrict__ w1, int d, int k, int H, uint2* __restrict__ Wf) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int KS = d / 16;
+  const int64_t total = (int64_t)(H / 8) * KS * 32;
+  if (idx >= total) return;
+  const int lane = (int)(idx & 31);
+  const int64_t q = idx >> 5;
+  const int ks = (int)(q % KS), nb = (int)(q / KS);
+  const int n = nb * 8 + lane / 4, k0 = ks * 16 + (lane % 4) * 2;
+  const float* row = w1 + (int64_t)n * (d + k);
+  __nv_bfloat162 lo = __floats2bfloat162_rn(row[k0], row[k0 + 1]);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(row[k0 + 8], row[k0 + 9]);
+  Wf[idx] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s) {
+  const int64_t total = (int64_t)(H / 8) * (d / 16) * 32;
+  k_prep_w1_frag<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(w1, d, k, H, reinterpret_cast<uint2*>(Wf));
+}
+
+size_t mlp_smem_bytes(int d, int k, int H, int L) {
+  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)PB * k + (size_t)PB * (H + 4) + (size_t)H * L);
+}
+
 void launch_mlp(const MlpArgs& a, cudaStream_t s) {
-  const int threads = a.H < 1024 ? a.H : 1024;
-  const size_t smem = sizeof(float) * ((size_t)a.d * PB + PB * a.k + (size_t)PB * a.H + (size_t)a.H * a.L);
+  const size_t smem = mlp_smem_bytes(a.d, a.k, a.H, a.L);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  k_mlp<<<(a.N + PB - 1) / PB, threads, smem, s>>>(a);
+  k_mlp<<<(a.N + PB - 1) / PB, MLP_THREADS, smem, s>>>(a);
 }
 
 }  // namespace argus

@@ -36,7 +36,8 @@ constexpr int STAGES = 24;
 constexpr int THREADS = 256;
 constexpr int ACC_COL0 = 384;            // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/;
+constexpr size_t SCRATCH_OFF = 1024;     // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + SCRATCH_OFF + 4 * 32 * 32 * 4;
 }  // namespace
 
 struct ScanSmem {  // placed after the stage ring
@@ -49,27 +50,48 @@ struct ScanSmem {  // placed after the stage ring
 };
 
 // Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
-// prompt: s = (acc * inv_c) * inv_q, threshold compare, rare register insert.
+// prompt.  Fast path (fully unrolled, no inserts): s = (acc * inv_c) * inv_q and a
+// candidate bit per column (s >= thr).  Slow path (rare, warp-uniform entry,
+// compact code): the warp parks its 32x32 scores in shared memory (column-major,
+// conflict-free) and each lane inserts its candidates into its register top-k.
 template <int KMAX>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&v)[32], const float4* __restrict__ icp, float iq, int c0,
-                                          int cmax, uint32_t g0, uint32_t world, TopList<KMAX>& tl, float& thr) {
+__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* __restrict__ icp, float iq, int c0,
+                                          int cmax, uint32_t g0, uint32_t world, TopList<KMAX>& tl, float& thr,
+                                          float* __restrict__ scratch) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mask = 0;
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     const float4 ic = __ldg(icp + c4);
-#define ARGUS_EPI(E, ICV)                                                                  \
-    {                                                                                      \
-      const int c = c0 + c4 * 4 + (E);                                                     \
-      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v[c4 * 4 + (E)]), (ICV)), iq);   \
-      if (s >= thr && c < cmax) {                                                          \
-        tl.insert(pack_key(s, g0 + (uint32_t)c * world));                                  \
-        if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);                          \
-      }                                                                                    \
+    const float icv0 = ic.x, icv1 = ic.y, icv2 = ic.z, icv3 = ic.w;
+#define ARGUS_EPI(E, ICV)                                                                   \
+    {                                                                                       \
+      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v[c4 * 4 + (E)]), (ICV)), iq);    \
+      v[c4 * 4 + (E)] = __float_as_uint(s);                                                 \
+      mask |= (s >= thr ? 1u : 0u) << (c4 * 4 + (E));                                      \
     }
-    ARGUS_EPI(0, ic.x)
-    ARGUS_EPI(1, ic.y)
-    ARGUS_EPI(2, ic.z)
-    ARGUS_EPI(3, ic.w)
+    ARGUS_EPI(0, icv0)
+    ARGUS_EPI(1, icv1)
+    ARGUS_EPI(2, icv2)
+    ARGUS_EPI(3, icv3)
 #undef ARGUS_EPI
+  }
+  const int lim = cmax - c0;  // columns >= lim are past the shard's last row
+  if (lim < 32) mask &= lim <= 0 ? 0u : ((1u << lim) - 1u);
+  if (__any_sync(0xffffffffu, mask != 0)) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) scratch[c * 32 + lane] = __uint_as_float(v[c]);
+    __syncwarp();
+    while (mask) {
+      const int c = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const float s = scratch[c * 32 + lane];
+      if (s >= thr) {
+        tl.insert(pack_key(s, g0 + (uint32_t)(c0 + c) * world));
+        if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -180,9 +202,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
+    float* scratch = reinterpret_cast<float*>(ring + (size_t)STAGES * STAGE_BYTES + SCRATCH_OFF) + q * 1024;
     TopList<KMAX> tl;
     tl.clear();
-    float thr = -INFINITY;
+    float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
     int64_t local = 0;
     for (int64_t t = t_begin; t < t_end; ++t, ++local) {
       __syncwarp();
@@ -197,13 +220,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::tmem_wait_ld();
       tc::fence_before();
       tc::mbar_arrive(tc::smem_u32(&sm->tempty[acc]));   // accumulator may be overwritten now
-      if (!active) continue;
+      if (!__any_sync(0xffffffffu, active)) continue;
       const float4* icp = reinterpret_cast<const float4*>(a.inv_c + j0);
       const int64_t rem_rows = a.m_local - j0;
       const int cmax = rem_rows < TN ? (int)rem_rows : TN;
       const uint32_t g0 = (uint32_t)(j0 * a.world + a.rank);
-      epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr);
-      epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr);
+      epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
+      epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
     }
     if (active) {
       uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;

@@ -49,7 +49,7 @@ void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint
 struct MlpArgs {
   const __nv_bfloat16* Xb;   // [n_pad][d]
   const float* topk_score;   // [N][k]
-  const __nv_bfloat16* W1xT; // [d][H]
+  const void* W1xF;          // W1x bf16 in mma.sync B-fragment order (see k_prep_w1_frag)
   const float* W1sT;         // [k][H]
   const float* b1;           // [H]
   const float* W2T;          // [H][L]
@@ -67,6 +67,9 @@ struct MlpArgs {
 };
 // K3 + A5: predictor MLP with fused compliance / preference / priority keys.
 void launch_mlp(const MlpArgs& a, cudaStream_t s);
+size_t mlp_smem_bytes(int d, int k, int H, int L);
+// init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
+void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
 
 struct AssignArgs {
   const uint8_t* pref;

@@ -266,6 +266,7 @@ class Problem:
     W2: np.ndarray
     b2: np.ndarray
     fractions: np.ndarray
+    k: int = 4
     extra: dict = field(default_factory=dict)
 
 
@@ -290,4 +291,4 @@ def small_problem(name="C1", N=None, M=None, d=None, k=None, seed=None, gates=Tr
             o["sim_gate"] = float("-inf")
     L = len(opts)
     W1, b1, W2, b2 = mlp_weights(d, k, cfg.hidden, L, stress=stress)
-    return Problem(cfg, cache, X, opts, W1, b1, W2, b2, load_fractions(L, cfg.frac_base))
+    return Problem(cfg, cache, X, opts, W1, b1, W2, b2, load_fractions(L, cfg.frac_base), k=k)

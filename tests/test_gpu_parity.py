@@ -25,7 +25,7 @@ def argus_mod():
 
 def make_router(argus, p, max_batch=None, capacity=None, **kw):
     N = p.X.shape[0]
-    return argus.Router(p.X.shape[1], p.cfg.k, p.opts, p.W1, p.b1, p.W2, p.b2,
+    return argus.Router(p.X.shape[1], p.k, p.opts, p.W1, p.b1, p.W2, p.b2,
                         capacity=capacity or max(p.cache.shape[0], 1) + 1024,
                         max_batch=max_batch or max(N, 1), **kw)
 
@@ -37,14 +37,14 @@ def run_case(argus, p, quota=None, check_e2e=True):
         if p.cache.shape[0]:
             assert r.argus_cache_insert(p.cache) == 0
         rc, g = r.argus_route_batch(p.X, quota)
-    tk = parity.check_topk(p.X, p.cache, p.cfg.k, g["topk_idx"], g["topk_score"])
+    tk = parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"])
     parity.check_mlp_replay(p.X, g, p.W1, p.b1, p.W2, p.b2)
     rep = parity.check_replay(g, p.opts, quota)
     assert rc == rep["rc"]
     parity.invariants(g, p.opts, quota)
     frac = None
     if check_e2e and p.cache.shape[0]:
-        ores = oracle.route(p.X, p.cache, p.cfg.k, p.W1, p.b1, p.W2, p.b2, p.opts, quota)
+        ores = oracle.route(p.X, p.cache, p.k, p.W1, p.b1, p.W2, p.b2, p.opts, quota)
         np.testing.assert_allclose(g["quality"], ores["rhat"], atol=parity.SCORE_TOL)   # M2
         frac = parity.check_e2e(ores, g, p.opts, quota)
     return g, tk, frac
@@ -128,7 +128,7 @@ def test_invalid_inputs(argus_mod):
             r.argus_cache_insert(zero)
         assert r.argus_cache_size() == 100         # failed inserts leave M unchanged
         rc, g = r.argus_route_batch(p.X, quota)    # router still usable
-        assert g["topk_idx"].shape == (4, p.cfg.k)
+        assert g["topk_idx"].shape == (4, p.k)
 
 
 def test_determinism(argus_mod):
@@ -150,7 +150,7 @@ def test_g_invariance_striped_shards(argus_mod):
     import torch
     argus = argus_mod
     p = gen.small_problem("C1", N=70, M=6001, seed=71)
-    N, k, L = 70, p.cfg.k, len(p.opts)
+    N, k, L = 70, p.k, len(p.opts)
     quota = oracle.quota_from_fractions(p.fractions, N)
     X = torch.from_numpy(p.X).cuda()
     ref = None
@@ -193,7 +193,7 @@ def test_g_invariance_striped_shards(argus_mod):
 def test_dev_path_matches_host_path(argus_mod):
     import torch
     p = gen.small_problem("C1", N=100, M=4500, seed=81)
-    N, k, L = 100, p.cfg.k, len(p.opts)
+    N, k, L = 100, p.k, len(p.opts)
     quota = oracle.quota_from_fractions(p.fractions, N)
     with make_router(argus_mod, p) as r:
         r.argus_cache_insert_dev(torch.from_numpy(p.cache).cuda())

@@ -115,6 +115,7 @@ struct argus_router {
   uint32_t* d_flags = nullptr;     // error / overflow flags
   uint32_t* h_flags = nullptr;     // pinned mirror
   CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
+  CUtensorMap tmap_q;              // TMA descriptor of the bf16 prompt batch (64x128 boxes, SW128)
   bool scan_simt = false;          // debug cross-check path (ARGUS_SCAN_SIMT=1)
   // stage profiling (argus_profile_*)
   bool prof = false;
@@ -183,7 +184,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 // TMA descriptor of the cache shard: bf16 [rows][d] row-major, box 64 (K) x 64 (rows),
 // 128-byte swizzle (matches the UMMA K-major SW128 shared-memory descriptor).
-static bool make_cache_tmap(CUtensorMap* m, void* base, int64_t rows, int d) {
+static bool make_tmap(CUtensorMap* m, void* base, int64_t rows, int d, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -194,7 +195,7 @@ static bool make_cache_tmap(CUtensorMap* m, void* base, int64_t rows, int d) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -451,7 +452,11 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_order, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_flags, 1));
   if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
-  if (!make_cache_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d)) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  if (!make_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d, 64) ||
+      !make_tmap(&r->tmap_q, r->d_Xb, r->n_pad_max, d, 128)) {
+    argus_route_destroy(r);
+    return ARGUS_E_CUDA;
+  }
   r->scan_simt = getenv("ARGUS_SCAN_SIMT") != nullptr;
   // zero the cache tail so TMA / vector loads past M never see garbage
   if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
@@ -642,7 +647,7 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
   {
     StageScope sc(r, ARGUS_STAGE_SCAN);
     if (r->scan_simt) launch_scan_simt(a, r->stream);
-    else launch_scan(a, &r->tmap_c, r->stream);
+    else launch_scan(a, &r->tmap_c, &r->tmap_q, r->stream);
   }
   LAUNCHED(r);
   {

@@ -12,10 +12,16 @@
 //   * the prompt slice is the UMMA A operand and lives in TMEM for the whole
 //     kernel (128 lanes x d/2 columns, loaded once with tcgen05.st);
 //   * cache tiles of 64 rows are the B operand: TMA (128-byte swizzle) streams
-//     64x64 bf16 boxes through a STAGES-deep mbarrier ring in shared memory;
+//     64x64 bf16 boxes into two tile buffers (d/64 boxes each, one mbarrier per
+//     box so the MMAs start as soon as the first box lands);
 //   * tcgen05.mma.cta_group::1.kind::f16, M=128 (prompts) x N=64 (cache rows) x
 //     K=16, issued by one thread into one of two TMEM accumulators
 //     (double-buffered, so the epilogue of tile t overlaps the MMAs of t+1);
+//     ONE tcgen05.commit per tile frees both the tile buffer and signals the
+//     accumulator (measured: a commit costs ~250 issue cycles, an N=64 MMA ~45,
+//     so per-k-block commits made the issue loop the bottleneck);
+//   * the prompt slice reaches TMEM through the tile buffers (one TMA burst, then
+//     shared memory -> registers -> tcgen05.st), not through dependent global loads;
 //   * epilogue: 4 warps, TMEM lane = prompt, so each thread owns ONE prompt and
 //     keeps its top-k in registers behind a float threshold: per score two
 //     FMULs, one compare; inserts are rare (~k ln(M/k) per prompt).
@@ -28,24 +34,26 @@
 namespace argus {
 
 namespace {
-constexpr int TN = 64;                   // cache rows per tile (UMMA N)
-constexpr int TM = 128;                  // prompts per CTA (UMMA M)
-constexpr int KBLK = 64;                 // bf16 per 128-byte swizzle row
-constexpr int STAGE_BYTES = TN * KBLK * 2;  // 8 KB
-constexpr int STAGES = 24;
+constexpr int TN = 64;                      // cache rows per tile (UMMA N)
+constexpr int TM = 128;                     // prompts per CTA (UMMA M)
+constexpr int KBLK = 64;                    // bf16 per 128-byte swizzle row
+constexpr int KB_MAX = 12;                  // d <= 768
+constexpr int BOX_BYTES = TN * KBLK * 2;    // 8 KB cache box
+constexpr int TILE_BYTES = KB_MAX * BOX_BYTES;  // 96 KB tile buffer
+constexpr int NBUF = 2;
 constexpr int THREADS = 256;
-constexpr int ACC_COL0 = 384;            // accumulators after the resident Q (d <= 768)
+constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SCRATCH_OFF = 1024;     // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + SCRATCH_OFF + 4 * 32 * 32 * 4;
+constexpr size_t SCRATCH_OFF = 1024;        // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
+constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + 4 * 32 * 32 * 4;
 }  // namespace
 
-struct ScanSmem {  // placed after the stage ring
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
-  uint64_t qready;
+struct ScanSmem {  // placed after the tile buffers
+  uint64_t full[NBUF][KB_MAX];  // TMA box landed
+  uint64_t done[NBUF];          // all MMAs of the tile in buffer b complete (one commit per tile)
+  uint64_t tempty[NBUF];        // epilogue has read accumulator b
+  uint64_t qfull;               // prompt slice landed in shared memory
+  uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
   uint32_t tmem_base;
 };
 
@@ -97,10 +105,11 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* __res
 
 template <int KMAX>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, ScanArgs a, int slices, int ranges, int64_t n_tiles) {
+    k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
+              int slices, int ranges, int64_t n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)STAGES * STAGE_BYTES);
+  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)NBUF * TILE_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x % slices;
   const int range = blockIdx.x / slices;
@@ -110,14 +119,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmap_c);
-    for (int s = 0; s < STAGES; ++s) {
-      tc::mbar_init(tc::smem_u32(&sm->full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->empty[s]), 1);
+    tc::prefetch_tmap(&tmap_q);
+    for (int b = 0; b < NBUF; ++b) {
+      for (int s = 0; s < KB_MAX; ++s) tc::mbar_init(tc::smem_u32(&sm->full[b][s]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->done[b]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 128);
     }
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(tc::smem_u32(&sm->tfull[s]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->tempty[s]), 128);
-    }
+    tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
     tc::mbar_init(tc::smem_u32(&sm->qready), 128);
     tc::fence_barrier_init();
   }
@@ -133,16 +141,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t t = t_begin; t < t_end; ++t) {
+      // prompt slice: KB boxes of 128 rows x 64 bf16 (16 KB, 128-byte swizzle) into the buffers
+      const uint32_t qb = tc::smem_u32(&sm->qfull);
+      tc::mbar_arrive_expect_tx(qb, (uint32_t)(KB * TM * KBLK * 2));
+      for (int kb = 0; kb < KB; ++kb)
+        tc::tma_load_2d(tc::smem_u32(ring + (size_t)kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
+      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // buffers free again
+      int64_t l = 0;
+      for (int64_t t = t_begin; t < t_end; ++t, ++l) {
+        const int b = (int)(l & 1);
+        if (l >= NBUF) tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)(((l - NBUF) >> 1) & 1));
+        uint8_t* buf = ring + (size_t)b * TILE_BYTES;
         for (int kb = 0; kb < KB; ++kb) {
-          tc::mbar_wait(tc::smem_u32(&sm->empty[stage]), phase ^ 1);
-          const uint32_t fb = tc::smem_u32(&sm->full[stage]);
-          tc::mbar_arrive_expect_tx(fb, STAGE_BYTES);
-          tc::tma_load_2d(tc::smem_u32(ring + (size_t)stage * STAGE_BYTES), &tmap_c, fb, kb * KBLK,
-                          (int32_t)(t * TN));
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          const uint32_t fb = tc::smem_u32(&sm->full[b][kb]);
+          tc::mbar_arrive_expect_tx(fb, BOX_BYTES);
+          tc::tma_load_2d(tc::smem_u32(buf + (size_t)kb * BOX_BYTES), &tmap_c, fb, kb * KBLK, (int32_t)(t * TN));
         }
       }
     }
@@ -152,74 +165,72 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
       tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
       tc::fence_after();
-      int stage = 0;
-      uint32_t phase = 0;
-      int64_t local = 0;
-      for (int64_t t = t_begin; t < t_end; ++t, ++local) {
-        const int acc = (int)(local & 1);
-        const uint32_t aphase = (uint32_t)((local >> 1) & 1);
-        tc::mbar_wait(tc::smem_u32(&sm->tempty[acc]), aphase ^ 1);
+      int64_t l = 0;
+      for (int64_t t = t_begin; t < t_end; ++t, ++l) {
+        const int b = (int)(l & 1);
+        const uint32_t ph = (uint32_t)((l >> 1) & 1);
+        tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), ph ^ 1);
         tc::fence_after();
-        const uint32_t d_tmem = tmem + ACC_COL0 + acc * TN;
+        const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
+        const uint32_t sbuf = tc::smem_u32(ring + (size_t)b * TILE_BYTES);
         for (int kb = 0; kb < KB; ++kb) {
-          tc::mbar_wait(tc::smem_u32(&sm->full[stage]), phase);
+          tc::mbar_wait(tc::smem_u32(&sm->full[b][kb]), ph);
           tc::fence_after();
-          const uint32_t sb = tc::smem_u32(ring + (size_t)stage * STAGE_BYTES);
+          const uint32_t sb = sbuf + kb * BOX_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk) {
-            const uint32_t a_tmem = tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8);
-            tc::mma_ts(d_tmem, a_tmem, tc::desc_kmajor_sw128(sb + kk * 32), IDESC, (kb | kk) != 0);
-          }
-          tc::mma_commit(tc::smem_u32(&sm->empty[stage]));  // frees the smem slot when these MMAs finish
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int kk = 0; kk < KBLK / 16; ++kk)
+            tc::mma_ts(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8), tc::desc_kmajor_sw128(sb + kk * 32),
+                       IDESC, (kb | kk) != 0);
         }
-        tc::mma_commit(tc::smem_u32(&sm->tfull[acc]));      // accumulator ready for the epilogue
+        tc::mma_commit(tc::smem_u32(&sm->done[b]));  // frees buffer b AND hands accumulator b to the epilogue
       }
     }
   } else if (warp >= 4) {
-    // ======================= Q load into TMEM (A operand), then the epilogue
+    // ======================= Q into TMEM (A operand), then the epilogue
     const int q = warp - 4;                 // TMEM lane quarter
     const int p_local = q * 32 + lane;      // prompt within the slice
     const int p = slice * TM + p_local;     // prompt within the batch
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     {
-      const uint4* src = reinterpret_cast<const uint4*>(a.Xb + (int64_t)p * a.d);  // rows >= N are zero
-      for (int c = 0; c < a.d / 64; ++c) {   // 64 bf16 = 32 TMEM columns per chunk
+      tc::mbar_wait(tc::smem_u32(&sm->qfull), 0);
+      const int sw = p_local & 7;  // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r % 8)
+      for (int c = 0; c < KB; ++c) {   // 64 bf16 = 32 TMEM columns per box
+        const uint8_t* row = ring + (size_t)c * TM * KBLK * 2 + (size_t)p_local * 128;
         uint32_t r[32];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const uint4 u = src[c * 8 + v];
-          r[4 * v + 0] = u.x;
-          r[4 * v + 1] = u.y;
-          r[4 * v + 2] = u.z;
-          r[4 * v + 3] = u.w;
+        for (int j = 0; j < 8; ++j) {
+          const uint4 u = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
+          r[4 * j + 0] = u.x;
+          r[4 * j + 1] = u.y;
+          r[4 * j + 2] = u.z;
+          r[4 * j + 3] = u.w;
         }
         tc::tmem_st32(tmem + lane_base + (uint32_t)(c * 32), r);
       }
       tc::tmem_wait_st();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc::fence_before();
       tc::mbar_arrive(tc::smem_u32(&sm->qready));
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    float* scratch = reinterpret_cast<float*>(ring + (size_t)STAGES * STAGE_BYTES + SCRATCH_OFF) + q * 1024;
+    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + q * 1024;
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
-    int64_t local = 0;
-    for (int64_t t = t_begin; t < t_end; ++t, ++local) {
+    int64_t l = 0;
+    for (int64_t t = t_begin; t < t_end; ++t, ++l) {
       __syncwarp();
-      const int acc = (int)(local & 1);
-      const uint32_t aphase = (uint32_t)((local >> 1) & 1);
+      const int b = (int)(l & 1);
       const int64_t j0 = t * TN;
-      tc::mbar_wait(tc::smem_u32(&sm->tfull[acc]), aphase);
+      tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
       tc::fence_after();
       uint32_t v0[32], v1[32];
-      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + acc * TN, v0);
-      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + acc * TN + 32, v1);
+      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN, v0);
+      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + 32, v1);
       tc::tmem_wait_ld();
       tc::fence_before();
-      tc::mbar_arrive(tc::smem_u32(&sm->tempty[acc]));   // accumulator may be overwritten now
+      tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));   // accumulator may be overwritten now
       if (!__any_sync(0xffffffffu, active)) continue;
       const float4* icp = reinterpret_cast<const float4*>(a.inv_c + j0);
       const int64_t rem_rows = a.m_local - j0;
@@ -253,9 +264,9 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
   return ranges;
 }
 
-bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / 2 <= ACC_COL0; }
+bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
-void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, cudaStream_t s) {
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s) {
   const int slices = (a.N + TM - 1) / TM;
   const int ranges = a.P;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
@@ -267,9 +278,9 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, cudaStream_t s) {
   }
   const dim3 grid(slices * ranges);
   if (a.k <= 4)
-    k_scan_tc<4><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, a, slices, ranges, n_tiles);
+    k_scan_tc<4><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, *tmap_q, a, slices, ranges, n_tiles);
   else
-    k_scan_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, a, slices, ranges, n_tiles);
+    k_scan_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, *tmap_q, a, slices, ranges, n_tiles);
 }
 
 }  // namespace argus

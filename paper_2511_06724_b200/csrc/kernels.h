@@ -36,7 +36,7 @@ void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
 int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);
 bool scan_supported(int d);
-void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, cudaStream_t s);
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q, cudaStream_t s);
 // SIMT reference-quality scan (debug cross-check only, ARGUS_SCAN_SIMT=1)
 int scan_plan_ranges_simt(int64_t m_local, int32_t N, int num_sms);
 void launch_scan_simt(const ScanArgs& a, cudaStream_t s);

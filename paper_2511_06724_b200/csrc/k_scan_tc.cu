@@ -44,7 +44,7 @@ constexpr int NBUF = 2;
 constexpr int THREADS = 256;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SCRATCH_OFF = 1024;        // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
+constexpr size_t SCRATCH_OFF = 2048;        // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
 constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + 4 * 32 * 32 * 4;
 }  // namespace
 
@@ -55,6 +55,8 @@ struct ScanSmem {  // placed after the tile buffers
   uint64_t qfull;               // prompt slice landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
   uint32_t tmem_base;
+  uint32_t pad_[3];
+  float invc[4][TN];            // inverse cache-row norms of tile l in slot l % 4 (bulk-copied with box 0)
 };
 
 // Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
@@ -63,14 +65,14 @@ struct ScanSmem {  // placed after the tile buffers
 // compact code): the warp parks its 32x32 scores in shared memory (column-major,
 // conflict-free) and each lane inserts its candidates into its register top-k.
 template <int KMAX>
-__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* __restrict__ icp, float iq, int c0,
+__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, float iq, int c0,
                                           int cmax, uint32_t g0, uint32_t world, TopList<KMAX>& tl, float& thr,
                                           float* __restrict__ scratch) {
   const int lane = threadIdx.x & 31;
   uint32_t mask = 0;
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
-    const float4 ic = __ldg(icp + c4);
+    const float4 ic = icp[c4];   // shared memory, same address in every lane (broadcast)
     const float icv0 = ic.x, icv1 = ic.y, icv2 = ic.z, icv3 = ic.w;
 #define ARGUS_EPI(E, ICV)                                                                   \
     {                                                                                       \
@@ -154,7 +156,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* buf = ring + (size_t)b * TILE_BYTES;
         for (int kb = 0; kb < KB; ++kb) {
           const uint32_t fb = tc::smem_u32(&sm->full[b][kb]);
-          tc::mbar_arrive_expect_tx(fb, BOX_BYTES);
+          tc::mbar_arrive_expect_tx(fb, BOX_BYTES + (kb == 0 ? TN * 4 : 0));
+          if (kb == 0)  // the tile's inverse norms ride on box 0's barrier (rows past capacity read zeros)
+            tc::bulk_load(tc::smem_u32(&sm->invc[l & 3][0]), a.inv_c + t * TN, TN * 4, fb);
           tc::tma_load_2d(tc::smem_u32(buf + (size_t)kb * BOX_BYTES), &tmap_c, fb, kb * KBLK, (int32_t)(t * TN));
         }
       }
@@ -224,20 +228,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN;
       tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
+      tc::mbar_wait(tc::smem_u32(&sm->full[b][0]), (uint32_t)((l >> 1) & 1));  // inv_c (already complete)
       tc::fence_after();
       uint32_t v0[32], v1[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN, v0);
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + 32, v1);
       tc::tmem_wait_ld();
+      if (__any_sync(0xffffffffu, active)) {
+        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & 3][0]);
+        const int64_t rem_rows = a.m_local - j0;
+        const int cmax = rem_rows < TN ? (int)rem_rows : TN;
+        const uint32_t g0 = (uint32_t)(j0 * a.world + a.rank);
+        epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
+        epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
+      }
+      // release accumulator b (and, transitively, inv_c slot l % 4) only after processing:
+      // MMA(l+2) waits for it, and the producer refills slot l % 4 only after done(l+2).
       tc::fence_before();
-      tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));   // accumulator may be overwritten now
-      if (!__any_sync(0xffffffffu, active)) continue;
-      const float4* icp = reinterpret_cast<const float4*>(a.inv_c + j0);
-      const int64_t rem_rows = a.m_local - j0;
-      const int cmax = rem_rows < TN ? (int)rem_rows : TN;
-      const uint32_t g0 = (uint32_t)(j0 * a.world + a.rank);
-      epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
-      epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
+      tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
     }
     if (active) {
       uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;

@@ -54,6 +54,7 @@ struct ScanSmem {  // placed after the tile buffers
   uint64_t tempty[NBUF];        // epilogue has read accumulator b
   uint64_t qfull;               // prompt slice landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
+  uint64_t invfull[4];          // inv_c slot l % 4 landed (cannot lap: refill needs this tile's release)
   uint32_t tmem_base;
   uint32_t pad_[3];
   float invc[4][TN];            // inverse cache-row norms of tile l in slot l % 4 (bulk-copied with box 0)
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 128);
     }
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
+    for (int s = 0; s < 4; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
     tc::mbar_init(tc::smem_u32(&sm->qready), 128);
     tc::fence_barrier_init();
   }
@@ -156,9 +158,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* buf = ring + (size_t)b * TILE_BYTES;
         for (int kb = 0; kb < KB; ++kb) {
           const uint32_t fb = tc::smem_u32(&sm->full[b][kb]);
-          tc::mbar_arrive_expect_tx(fb, BOX_BYTES + (kb == 0 ? TN * 4 : 0));
-          if (kb == 0)  // the tile's inverse norms ride on box 0's barrier (rows past capacity read zeros)
-            tc::bulk_load(tc::smem_u32(&sm->invc[l & 3][0]), a.inv_c + t * TN, TN * 4, fb);
+          tc::mbar_arrive_expect_tx(fb, BOX_BYTES);
+          if (kb == 0) {  // the tile's inverse norms (rows past capacity read zeros)
+            const uint32_t ib = tc::smem_u32(&sm->invfull[l & 3]);
+            tc::mbar_arrive_expect_tx(ib, TN * 4);
+            tc::bulk_load(tc::smem_u32(&sm->invc[l & 3][0]), a.inv_c + t * TN, TN * 4, ib);
+          }
           tc::tma_load_2d(tc::smem_u32(buf + (size_t)kb * BOX_BYTES), &tmap_c, fb, kb * KBLK, (int32_t)(t * TN));
         }
       }
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN;
       tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
-      tc::mbar_wait(tc::smem_u32(&sm->full[b][0]), (uint32_t)((l >> 1) & 1));  // inv_c (already complete)
+      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & 3]), (uint32_t)((l >> 2) & 1));
       tc::fence_after();
       uint32_t v0[32], v1[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN, v0);

@@ -209,3 +209,17 @@ def test_dev_path_matches_host_path(argus_mod):
     np.testing.assert_array_equal(o["option"].cpu().numpy(), g["option"])
     np.testing.assert_array_equal(o["topk_idx"].cpu().numpy().view(np.uint32), g["topk_idx"])
     np.testing.assert_array_equal(o["quality"].cpu().numpy(), g["quality"])
+
+
+@pytest.mark.parametrize("N,M,seed", [(70, 60000, 91), (300, 30000, 92), (129, 40000, 93)])
+def test_many_tiles_per_cta(argus_mod, N, M, seed):
+    """Every CTA walks many cache tiles (buffer / accumulator / barrier phases wrap
+    several times), including the multi-slice (N > 128) launch."""
+    p = gen.small_problem("C2", N=N, M=M, seed=seed)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    with make_router(argus_mod, p) as r:
+        r.argus_cache_insert(p.cache)
+        rc, g = r.argus_route_batch(p.X, quota)
+    parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"])
+    parity.check_replay(g, p.opts, quota)
+    parity.invariants(g, p.opts, quota)

@@ -41,15 +41,16 @@ constexpr int KB_MAX = 12;                  // d <= 768
 constexpr int BOX_BYTES = TN * KBLK * 2;    // 8 KB cache box
 constexpr int TILE_BYTES = KB_MAX * BOX_BYTES;  // 96 KB tile buffer
 constexpr int NBUF = 2;
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;               // 4 control warps + 8 epilogue warps
+constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SCRATCH_OFF = 2048;        // after the barriers: 4 warps x 32 x 32 fp32 slow-path scratch
-constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + 4 * 32 * 32 * 4;
+constexpr size_t SCRATCH_OFF = 2048;        // after the barriers: 8 warps x 32 x 32 fp32 slow-path scratch
+constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 32 * 32 * 4;
 }  // namespace
 
 struct ScanSmem {  // placed after the tile buffers
-  uint64_t full[NBUF][KB_MAX];  // TMA box landed
+  uint64_t full[NBUF];          // all TMA boxes of the tile in buffer b landed
   uint64_t done[NBUF];          // all MMAs of the tile in buffer b complete (one commit per tile)
   uint64_t tempty[NBUF];        // epilogue has read accumulator b
   uint64_t qfull;               // prompt slice landed in shared memory
@@ -61,45 +62,42 @@ struct ScanSmem {  // placed after the tile buffers
 };
 
 // Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
-// prompt.  Fast path (fully unrolled, no inserts): s = (acc * inv_c) * inv_q and a
-// candidate bit per column (s >= thr).  Slow path (rare, warp-uniform entry,
-// compact code): the warp parks its 32x32 scores in shared memory (column-major,
-// conflict-free) and each lane inserts its candidates into its register top-k.
+// prompt.  Fast path (2 instructions per score): x_c = acc_c * inv_c[c] and a
+// running max; since rounding is monotone, max_c fl(x_c * inv_q) = fl(max_c x_c *
+// inv_q), so the chunk holds a candidate iff fl(max * inv_q) >= thr.  Slow path
+// (warp-uniform entry, compact code): the warp parks its 32x32 x values in shared
+// memory (column-major, conflict-free) and each lane rescans its own 32 with the
+// exact score s = fl(x * inv_q) and inserts into its register top-k.
 template <int KMAX>
-__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, float iq, int c0,
-                                          int cmax, uint32_t g0, uint32_t world, TopList<KMAX>& tl, float& thr,
+__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, float iq, int cmax, uint32_t g0,
+                                          uint32_t world, TopList<KMAX>& tl, float& thr,
                                           float* __restrict__ scratch) {
   const int lane = threadIdx.x & 31;
-  uint32_t mask = 0;
+  float m = -INFINITY;
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     const float4 ic = icp[c4];   // shared memory, same address in every lane (broadcast)
-    const float icv0 = ic.x, icv1 = ic.y, icv2 = ic.z, icv3 = ic.w;
-#define ARGUS_EPI(E, ICV)                                                                   \
-    {                                                                                       \
-      const float s = __fmul_rn(__fmul_rn(__uint_as_float(v[c4 * 4 + (E)]), (ICV)), iq);    \
-      v[c4 * 4 + (E)] = __float_as_uint(s);                                                 \
-      mask |= (s >= thr ? 1u : 0u) << (c4 * 4 + (E));                                      \
-    }
-    ARGUS_EPI(0, icv0)
-    ARGUS_EPI(1, icv1)
-    ARGUS_EPI(2, icv2)
-    ARGUS_EPI(3, icv3)
-#undef ARGUS_EPI
+    const float x0 = __fmul_rn(__uint_as_float(v[c4 * 4 + 0]), ic.x);
+    const float x1 = __fmul_rn(__uint_as_float(v[c4 * 4 + 1]), ic.y);
+    const float x2 = __fmul_rn(__uint_as_float(v[c4 * 4 + 2]), ic.z);
+    const float x3 = __fmul_rn(__uint_as_float(v[c4 * 4 + 3]), ic.w);
+    v[c4 * 4 + 0] = __float_as_uint(x0);
+    v[c4 * 4 + 1] = __float_as_uint(x1);
+    v[c4 * 4 + 2] = __float_as_uint(x2);
+    v[c4 * 4 + 3] = __float_as_uint(x3);
+    m = fmaxf(m, fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)));
   }
-  const int lim = cmax - c0;  // columns >= lim are past the shard's last row
-  if (lim < 32) mask &= lim <= 0 ? 0u : ((1u << lim) - 1u);
-  if (__any_sync(0xffffffffu, mask != 0)) {
+  const bool cand = __fmul_rn(m, iq) >= thr;
+  if (__any_sync(0xffffffffu, cand)) {
+    if (cand) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) scratch[c * 32 + lane] = __uint_as_float(v[c]);
-    __syncwarp();
-    while (mask) {
-      const int c = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const float s = scratch[c * 32 + lane];
-      if (s >= thr) {
-        tl.insert(pack_key(s, g0 + (uint32_t)(c0 + c) * world));
-        if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+      for (int c = 0; c < 32; ++c) scratch[c * 32 + lane] = __uint_as_float(v[c]);
+      for (int c = 0; c < cmax; ++c) {
+        const float s = __fmul_rn(scratch[c * 32 + lane], iq);
+        if (s >= thr) {
+          tl.insert(pack_key(s, g0 + (uint32_t)c * world));
+          if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+        }
       }
     }
     __syncwarp();
@@ -124,13 +122,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::prefetch_tmap(&tmap_c);
     tc::prefetch_tmap(&tmap_q);
     for (int b = 0; b < NBUF; ++b) {
-      for (int s = 0; s < KB_MAX; ++s) tc::mbar_init(tc::smem_u32(&sm->full[b][s]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->full[b]), 1);
       tc::mbar_init(tc::smem_u32(&sm->done[b]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 128);
+      tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 32 * EPI_WARPS);
     }
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
     for (int s = 0; s < 4; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
-    tc::mbar_init(tc::smem_u32(&sm->qready), 128);
+    tc::mbar_init(tc::smem_u32(&sm->qready), 32 * EPI_WARPS);
     tc::fence_barrier_init();
   }
   if (warp == 2) {
@@ -156,9 +154,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int b = (int)(l & 1);
         if (l >= NBUF) tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)(((l - NBUF) >> 1) & 1));
         uint8_t* buf = ring + (size_t)b * TILE_BYTES;
+        const uint32_t fb = tc::smem_u32(&sm->full[b]);
+        tc::mbar_arrive_expect_tx(fb, (uint32_t)(KB * BOX_BYTES));
         for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t fb = tc::smem_u32(&sm->full[b][kb]);
-          tc::mbar_arrive_expect_tx(fb, BOX_BYTES);
           if (kb == 0) {  // the tile's inverse norms (rows past capacity read zeros)
             const uint32_t ib = tc::smem_u32(&sm->invfull[l & 3]);
             tc::mbar_arrive_expect_tx(ib, TN * 4);
@@ -182,9 +180,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::fence_after();
         const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
         const uint32_t sbuf = tc::smem_u32(ring + (size_t)b * TILE_BYTES);
+        tc::mbar_wait(tc::smem_u32(&sm->full[b]), ph);
+        tc::fence_after();
         for (int kb = 0; kb < KB; ++kb) {
-          tc::mbar_wait(tc::smem_u32(&sm->full[b][kb]), ph);
-          tc::fence_after();
           const uint32_t sb = sbuf + kb * BOX_BYTES;
 #pragma unroll
           for (int kk = 0; kk < KBLK / 16; ++kk)
@@ -196,14 +194,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= 4) {
     // ======================= Q into TMEM (A operand), then the epilogue
-    const int q = warp - 4;                 // TMEM lane quarter
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    const int h = (warp - 4) >> 2;          // column half of every tile (32 of the 64 cache rows)
     const int p_local = q * 32 + lane;      // prompt within the slice
     const int p = slice * TM + p_local;     // prompt within the batch
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     {
       tc::mbar_wait(tc::smem_u32(&sm->qfull), 0);
       const int sw = p_local & 7;  // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r % 8)
-      for (int c = 0; c < KB; ++c) {   // 64 bf16 = 32 TMEM columns per box
+      for (int c = h; c < KB; c += 2) {   // 64 bf16 = 32 TMEM columns per box; halves split the boxes
         const uint8_t* row = ring + (size_t)c * TM * KBLK * 2 + (size_t)p_local * 128;
         uint32_t r[32];
 #pragma unroll
@@ -223,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + q * 1024;
+    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + (warp - 4) * 1024;
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
@@ -231,21 +230,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t t = t_begin; t < t_end; ++t, ++l) {
       __syncwarp();
       const int b = (int)(l & 1);
-      const int64_t j0 = t * TN;
+      const int64_t j0 = t * TN + h * 32;
       tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & 3]), (uint32_t)((l >> 2) & 1));
       tc::fence_after();
-      uint32_t v0[32], v1[32];
-      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN, v0);
-      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + 32, v1);
+      uint32_t v[32];
+      tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + h * 32, v);
       tc::tmem_wait_ld();
       if (__any_sync(0xffffffffu, active)) {
-        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & 3][0]);
+        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & 3][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
-        const int cmax = rem_rows < TN ? (int)rem_rows : TN;
-        const uint32_t g0 = (uint32_t)(j0 * a.world + a.rank);
-        epi_chunk<KMAX>(v0, icp, iq, 0, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
-        epi_chunk<KMAX>(v1, icp + 8, iq, 32, cmax, g0, (uint32_t)a.world, tl, thr, scratch);
+        const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
+        epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
       }
       // release accumulator b (and, transitively, inv_c slot l % 4) only after processing:
       // MMA(l+2) waits for it, and the producer refills slot l % 4 only after done(l+2).
@@ -253,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
     }
     if (active) {
-      uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
+      uint64_t* out = a.partial + ((int64_t)(range * 2 + h) * a.N + p) * a.k;
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2)
         if (t2 < a.k) out[t2] = tl.v[t2];
@@ -274,14 +270,14 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
   if (ranges < 1) ranges = 1;
   const int64_t n_tiles = (m_local + TN - 1) / TN;
   if (ranges > n_tiles) ranges = (int)(n_tiles > 0 ? n_tiles : 1);
-  return ranges;
+  return 2 * ranges;  // partial lists: one per (range, column half)
 }
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s) {
   const int slices = (a.N + TM - 1) / TM;
-  const int ranges = a.P;
+  const int ranges = a.P / 2;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   static bool attr = false;
   if (!attr) {

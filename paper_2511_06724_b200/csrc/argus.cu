@@ -91,7 +91,9 @@ struct argus_router {
   __nv_bfloat16* d_W1xF = nullptr;  // [H*d] bf16, mma fragment order
   float* d_W1sT = nullptr;
   float* d_b1 = nullptr;
-  float* d_W2T = nullptr;
+  float* d_W2 = nullptr;           // [L][H]
+  float* d_h = nullptr;            // [n16][H] predictor hidden activations
+  int32_t* d_mlp_cnt = nullptr;    // [n16 / 16] last-CTA tickets
   float* d_b2 = nullptr;
   // cache shard (device)
   __nv_bfloat16* d_Cb = nullptr;
@@ -106,7 +108,7 @@ struct argus_router {
   float* d_score = nullptr;        // [max_batch][k]
   uint32_t* d_idx = nullptr;       // [max_batch][k]
   float* d_rhat = nullptr;         // [max_batch][L]
-  uint8_t* d_pref = nullptr;       // [max_batch][L]
+  uint8_t* d_pref = nullptr;       // [max_batch][L] rank of option v in pi_i
   uint8_t* d_ccount = nullptr;     // [max_batch]
   uint32_t* d_cmask = nullptr;     // [max_batch]
   uint8_t* d_status = nullptr;     // [max_batch]
@@ -164,17 +166,12 @@ static int dalloc(argus_router* r, T** p, size_t n) {
 static bool nccl_mode(const argus_router* r) { return r->cfg.world > 1 && r->comm != nullptr; }
 
 // transpose / round the predictor weights on the device (init time)
-__global__ void k_prep_weights(const float* __restrict__ w1, const float* __restrict__ w2, int d, int k,
-                               int H, int L, float* __restrict__ W1sT, float* __restrict__ W2T) {
+__global__ void k_prep_weights(const float* __restrict__ w1, int d, int k, int H, float* __restrict__ W1sT) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = (int64_t)H * (d + k);
   if (tid < n1) {
     const int j = (int)(tid / (d + k)), c = (int)(tid % (d + k));
     if (c >= d) W1sT[(int64_t)(c - d) * H + j] = w1[tid];
-  } else if (tid < n1 + (int64_t)L * H) {
-    const int64_t t = tid - n1;
-    const int v = (int)(t / H), j = (int)(t % H);
-    W2T[(int64_t)j * L + v] = w2[t];
   }
 }
 
@@ -347,7 +344,7 @@ int argus_route_destroy(argus_router* r) {
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
   void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xF,  r->d_W1sT,     r->d_b1,
-                  r->d_W2T,   r->d_b2,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
+                  r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
                   r->d_order, r->d_flags};
@@ -431,7 +428,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_W1xF, (size_t)d * H));
   TRY_RC(dalloc(r, &r->d_W1sT, (size_t)k * H));
   TRY_RC(dalloc(r, &r->d_b1, H));
-  TRY_RC(dalloc(r, &r->d_W2T, (size_t)H * L));
+  TRY_RC(dalloc(r, &r->d_W2, (size_t)H * L));
+  const int64_t n16 = ((int64_t)c.max_batch + 15) / 16 * 16;
+  TRY_RC(dalloc(r, &r->d_h, (size_t)n16 * H));
+  TRY_RC(dalloc(r, &r->d_mlp_cnt, (size_t)n16 / 16));
   TRY_RC(dalloc(r, &r->d_b2, L));
   TRY_RC(dalloc(r, &r->d_Cb, (size_t)(r->cap_local + 256) * d));
   TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
@@ -461,7 +461,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   // zero the cache tail so TMA / vector loads past M never see garbage
   if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
-      cudaMemsetAsync(r->d_flags, 0, sizeof(uint32_t), r->stream) != cudaSuccess) {
+      cudaMemsetAsync(r->d_flags, 0, sizeof(uint32_t), r->stream) != cudaSuccess ||
+      cudaMemsetAsync(r->d_mlp_cnt, 0, sizeof(int32_t) * (size_t)(n16 / 16), r->stream) != cudaSuccess) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
@@ -477,10 +478,9 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     }
   }
   float* d_w1 = nullptr;
-  float* d_w2 = nullptr;
+  float* d_w2 = r->d_W2;  // W2 is used in its caller layout [L][H]
   TRY_RC(dalloc(r, &d_w1, (size_t)H * (d + k)));
-  TRY_RC(dalloc(r, &d_w2, (size_t)L * H));
-  auto cleanup_tmp = [&]() { cudaFree(d_w1); cudaFree(d_w2); };
+  auto cleanup_tmp = [&]() { cudaFree(d_w1); };
   if (root_data) {
     if (cudaMemcpy(r->d_kskip, ks.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(r->d_pth, pth.data(), 4 * L, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -510,9 +510,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     }
   }
   {
-    const int64_t tot = (int64_t)H * (d + k) + (int64_t)L * H;
-    k_prep_weights<<<(unsigned)((tot + 255) / 256), 256, 0, r->stream>>>(d_w1, d_w2, d, k, H, L, r->d_W1sT,
-                                                                          r->d_W2T);
+    const int64_t tot = (int64_t)H * (d + k);
+    k_prep_weights<<<(unsigned)((tot + 255) / 256), 256, 0, r->stream>>>(d_w1, d, k, H, r->d_W1sT);
     launch_prep_w1_frag(d_w1, d, k, H, r->d_W1xF, r->stream);
     r->launches += 2;
   }
@@ -608,7 +607,15 @@ static int64_t local_rows(const argus_router* r) {
   return (r->m_global + G - 1 - rk) / G;
 }
 
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, uint32_t* idx_dev,
+                        float* score_dev);
+
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
+  return partial_impl(r, prompts_dev, N, keys_dev, nullptr, nullptr);
+}
+
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, uint32_t* idx_dev,
+                        float* score_dev) {
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch || !keys_dev) return ARGUS_E_INVALID;
@@ -652,15 +659,27 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
   LAUNCHED(r);
   {
     StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
-    launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
+    launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, idx_dev, score_dev, r->stream);
   }
   LAUNCHED(r);
   return ARGUS_OK;
 }
 
+static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N, const int32_t* quota,
+                       int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
+                       uint8_t* status_dev, bool merged);
+
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
                            float* topk_score_dev, float* quality_dev, uint8_t* status_dev) {
+  return finish_impl(r, keys_all_dev, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
+                     status_dev, false);
+}
+
+// merged: the single-shard path already decoded ids / scores in its local merge.
+static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N, const int32_t* quota,
+                       int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
+                       uint8_t* status_dev, bool merged) {
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch || G < 1 || !keys_all_dev || !quota) return ARGUS_E_INVALID;
@@ -673,18 +692,22 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   float* score = topk_score_dev ? topk_score_dev : r->d_score;
   uint32_t* idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
-  {
-    StageScope sc(r, ARGUS_STAGE_MERGE_GLOBAL);
-    launch_merge_topk(keys_all_dev, G, N, k, r->d_keys, idx, score, r->stream);
+  if (!merged) {
+    {
+      StageScope sc(r, ARGUS_STAGE_MERGE_GLOBAL);
+      launch_merge_topk(keys_all_dev, G, N, k, r->d_keys, idx, score, r->stream);
+    }
+    LAUNCHED(r);
   }
-  LAUNCHED(r);
   MlpArgs m{};
   m.Xb = r->d_Xb;
   m.topk_score = score;
   m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;
-  m.W2T = r->d_W2T;
+  m.W2 = r->d_W2;
+  m.hbuf = r->d_h;
+  m.block_cnt = r->d_mlp_cnt;
   m.b2 = r->d_b2;
   m.kskip = r->d_kskip;
   m.pth = r->d_pth;
@@ -696,7 +719,7 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
   m.H = r->cfg.hidden;
   m.L = L;
   m.rhat = quality_dev ? quality_dev : r->d_rhat;
-  m.pref = r->d_pref;
+  m.rankof = r->d_pref;
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
   uint8_t* status = status_dev ? status_dev : r->d_status;
@@ -707,7 +730,7 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
   }
   LAUNCHED(r);
   AssignArgs as{};
-  as.pref = r->d_pref;
+  as.rankof = r->d_pref;
   as.ccount = r->d_ccount;
   as.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
@@ -736,17 +759,18 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     return ARGUS_E_INVALID;
   for (int v = 0; v < r->cfg.L; ++v)
     if (quota[v] < 0) return ARGUS_E_INVALID;
-  rc = argus_route_partial_dev(r, prompts_dev, N, r->d_keys);
-  if (rc) return rc;
-  const uint64_t* all = r->d_keys;
-  int G = 1;
-  if (nccl_mode(r)) {  // C-2: N*k candidate keys from every shard
-    NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
-    all = r->d_keys_all;
-    G = r->cfg.world;
+  if (!nccl_mode(r)) {  // single shard: the local merge is final and decodes ids / scores directly
+    rc = partial_impl(r, prompts_dev, N, r->d_keys, topk_idx_dev, topk_score_dev);
+    if (rc) return rc;
+    return finish_impl(r, r->d_keys, 1, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
+                       status_dev, true);
   }
-  return argus_route_finish_dev(r, all, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
-                                quality_dev, status_dev);
+  rc = partial_impl(r, prompts_dev, N, r->d_keys, nullptr, nullptr);
+  if (rc) return rc;
+  // C-2: N*k candidate keys from every shard
+  NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
+  return finish_impl(r, r->d_keys_all, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
+                     quality_dev, status_dev, false);
 }
 
 int argus_sync(argus_router* r) {

@@ -8,21 +8,24 @@
 //   C_i = {v in A_i : r_v >= delta}                     (reading R6)
 //   pi_i = A_i sorted by (r desc, p_th desc, v asc)     (reading R13)
 //
-// One CTA = 8 warps x 16 prompts.  Layer 1 is a [16 x d] x [d x H] bf16 product
-// on the tensor cores (mma.sync m16n8k16, fp32 accumulate; <0.03 % of the
-// scan's flops, so the legacy warp-level MMA is the right size here): the prompt
-// block sits in shared memory (padded rows, conflict-free fragment loads) and
-// W1x is pre-arranged at init in per-lane fragment order so each B fragment is
-// one coalesced 8-byte load.  Layer 2 + A5 run one warp per prompt with lane v
-// owning option v (L <= 32), so masks are ballots and the preference rank is a
-// 32-lane compare-count.
+// Grid = (prompt blocks of 16) x (hidden chunks of 32): a small batch still
+// spreads over many SMs.  Layer 1 per CTA is a [16 x d] x [d x 32] bf16 product
+// on the tensor cores (mma.sync m16n8k16, fp32 accumulate; the whole predictor is
+// < 0.03 % of the scan's flops), split over 8 warps along d and reduced in shared
+// memory.  W1x is pre-arranged at init in per-lane fragment order so each B
+// fragment is one coalesced 8-byte load.  The last CTA of a prompt block (atomic
+// ticket) runs layer 2 + A5 for its 16 prompts: one warp per prompt, lanes split
+// the hidden units, lane v finally owns option v (L <= 32), so masks are ballots
+// and the preference rank is a 32-lane compare-count (stored per option: the
+// inverse permutation of pi_i, which is what the assignment walk consumes).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace argus {
 
-constexpr int PB = 16;  // prompts per CTA (the MMA M dimension)
+constexpr int PB = 16;  // prompts per block (the MMA M dimension)
 constexpr int MLP_THREADS = 256;
+constexpr int MLP_WARPS = MLP_THREADS / 32;
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint2 b) {
   asm volatile(
@@ -34,18 +37,17 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
 
 __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
+  __shared__ int is_last;
   const int d = a.d, H = a.H, L = a.L, k = a.k;
-  const int RS = d + 8;                                              // padded bf16 row stride
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smraw);       // [PB][RS]
-  float* ss = reinterpret_cast<float*>(smraw + (size_t)PB * RS * 2);  // [PB][k]
-  float* hs = ss + PB * k;                                           // [PB][H + 4]
-  float* w2 = hs + (size_t)PB * (H + 4);                             // [H][L]
-  const int HS = H + 4;
-  const int i0 = blockIdx.x * PB;
+  const int RS = d + 8;                                               // padded bf16 row stride
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smraw);        // [PB][RS]
+  float* red = reinterpret_cast<float*>(smraw + (size_t)PB * RS * 2);  // [MLP_WARPS][PB*32]
+  float* ss = red + MLP_WARPS * PB * 32;                              // [PB][k]
+  const int pb = blockIdx.x, cc = blockIdx.y;
+  const int i0 = pb * PB;
   const int nP = min(PB, a.N - i0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // prompt block (bf16) -> shared; rows past N are zero
   for (int idx = tid; idx < PB * (d / 8); idx += MLP_THREADS) {
     const int p = idx / (d / 8), c = idx - p * (d / 8);
     uint4 u = make_uint4(0, 0, 0, 0);
@@ -56,64 +58,95 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
     const int p = idx / k;
     ss[idx] = p < nP ? a.topk_score[(int64_t)(i0 + p) * k + (idx - p * k)] : 0.f;
   }
-  for (int idx = tid; idx < H * L; idx += MLP_THREADS) w2[idx] = a.W2T[idx];
   __syncthreads();
 
-  // ---- layer 1 on the tensor cores: warp -> 32 hidden units per pass
-  const int g = lane >> 2, t = lane & 3;
-  const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
-  const int RSW = RS / 2;  // row stride in 32-bit words
-  const int KS = d / 16;
-  const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
-  for (int cc = warp; cc < H / 32; cc += MLP_THREADS / 32) {
+  // ---- layer 1, hidden units [32 cc, 32 cc + 32), warp w takes a 1/8 slice of d
+  {
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
+    const int RSW = RS / 2;
+    const int KS = d / 16;
+    const int ks0 = KS * warp / MLP_WARPS, ks1 = KS * (warp + 1) / MLP_WARPS;
+    const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
     float acc[4][4];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-#pragma unroll 4
-    for (int ks = 0; ks < KS; ++ks) {
+#pragma unroll 2
+    for (int ks = ks0; ks < ks1; ++ks) {
+      uint2 bf[4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks) * 32 + lane);
       uint32_t af[4];
       af[0] = x32[g * RSW + ks * 8 + t];
       af[1] = x32[(g + 8) * RSW + ks * 8 + t];
       af[2] = x32[g * RSW + ks * 8 + 4 + t];
       af[3] = x32[(g + 8) * RSW + ks * 8 + 4 + t];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int nb = cc * 4 + nt;
-        const uint2 b = __ldg(wf + ((int64_t)nb * KS + ks) * 32 + lane);
-        mma_bf16_16816(acc[nt], af, b);
-      }
+      for (int nt = 0; nt < 4; ++nt) mma_bf16_16816(acc[nt], af, bf[nt]);
     }
-    // epilogue: + W1s . s + b1, relu -> hs
+    float* rw = red + warp * PB * 32;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int row = g + (e >> 1) * 8;
-        const int j = (cc * 4 + nt) * 8 + 2 * t + (e & 1);
-        float z = acc[nt][e];
-        for (int q = 0; q < k; ++q) z = __fmaf_rn(a.W1sT[q * H + j], ss[row * k + q], z);
-        hs[row * HS + j] = fmaxf(__fadd_rn(z, a.b1[j]), 0.f);
-      }
-    }
+      for (int e = 0; e < 4; ++e) rw[(g + (e >> 1) * 8) * 32 + nt * 8 + 2 * t + (e & 1)] = acc[nt][e];
   }
   __syncthreads();
+  // reduce the 8 split-K partials (fixed order), + W1s . s + b1, relu -> h (global)
+  for (int e = tid; e < PB * 32; e += MLP_THREADS) {
+    const int row = e >> 5, jl = e & 31, j = cc * 32 + jl;
+    float z = 0.f;
+#pragma unroll
+    for (int w = 0; w < MLP_WARPS; ++w) z = __fadd_rn(z, red[w * PB * 32 + e]);
+    for (int q = 0; q < k; ++q) z = __fmaf_rn(a.W1sT[q * H + j], ss[row * k + q], z);
+    a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, a.b1[j]), 0.f);
+  }
+  // ---- the last CTA of this prompt block runs layer 2 + A5
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int ticket = atomicAdd(&a.block_cnt[pb], 1);
+    is_last = ticket == (int)gridDim.y - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (tid == 0) a.block_cnt[pb] = 0;  // ready for the next launch
+  float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]  (reuses the staging area)
+  for (int e = tid; e < PB * H; e += MLP_THREADS) hs[e] = __ldcg(a.hbuf + (int64_t)i0 * H + e);
+  __syncthreads();
 
-  // ---- layer 2 + A5: warp per prompt, lane v = option v
-  for (int p = warp; p < nP; p += MLP_THREADS / 32) {
+  for (int p = warp; p < nP; p += MLP_WARPS) {
     const int i = i0 + p;
     const bool act = lane < L;
+    // z_v = b2_v + sum_j W2[v][j] h_j: lanes split j, butterfly-reduce per option
+    float part[32];
+#pragma unroll
+    for (int v = 0; v < 32; ++v) part[v] = 0.f;
+    for (int j = lane; j < H; j += 32) {
+      const float hj = hs[p * H + j];
+#pragma unroll
+      for (int v = 0; v < 32; ++v)
+        if (v < L) part[v] = __fmaf_rn(__ldg(a.W2 + (int64_t)v * H + j), hj, part[v]);
+    }
+    float z = 0.f;
+#pragma unroll
+    for (int v = 0; v < 32; ++v) {
+      if (v < L) {
+        float sv = part[v];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, m));
+        if (lane == v) z = sv;
+      }
+    }
     float r = 0.f;
     if (act) {
-      float z = a.b2[lane];
-      const float* hp = hs + p * HS;
-#pragma unroll 8
-      for (int j = 0; j < H; ++j) z = __fmaf_rn(w2[j * L + lane], hp[j], z);
+      z = __fadd_rn(z, a.b2[lane]);
       r = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
       if (lane == 0) r = 1.0f;
     }
-    const float s1 = ss[p * k];
+    const float s1 = __ldcg(a.topk_score + (int64_t)i * k);
     const int ks_ = act ? a.kskip[lane] : 0;
     const float gate = act ? a.gate[lane] : 0.f;
     const bool gated_pass = act && ks_ != 0 && s1 >= gate;
@@ -134,10 +167,8 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
     }
     if (act) {
       a.rhat[(int64_t)i * L + lane] = r;
-      a.pref[(int64_t)i * L + lane] = 0xFF;
+      a.rankof[(int64_t)i * L + lane] = adm ? (uint8_t)rank : (uint8_t)0xFF;  // position of v in pi_i
     }
-    __syncwarp();
-    if (adm) a.pref[(int64_t)i * L + rank] = (uint8_t)lane;
     if (lane == 0) {
       a.ccount[i] = (uint8_t)__popc(cmask);
       a.cmask[i] = cmask;
@@ -170,7 +201,10 @@ void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStr
 }
 
 size_t mlp_smem_bytes(int d, int k, int H, int L) {
-  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)PB * k + (size_t)PB * (H + 4) + (size_t)H * L);
+  (void)L;
+  const size_t phase1 = (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)MLP_WARPS * PB * 32 + (size_t)PB * k);
+  const size_t phase2 = sizeof(float) * (size_t)PB * H;
+  return phase1 > phase2 ? phase1 : phase2;
 }
 
 void launch_mlp(const MlpArgs& a, cudaStream_t s) {
@@ -180,7 +214,8 @@ void launch_mlp(const MlpArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  k_mlp<<<(a.N + PB - 1) / PB, MLP_THREADS, smem, s>>>(a);
+  const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
+  k_mlp<<<grid, MLP_THREADS, smem, s>>>(a);
 }
 
 }  // namespace argus

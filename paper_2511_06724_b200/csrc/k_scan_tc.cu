@@ -45,7 +45,8 @@ constexpr int THREADS = 384;               // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SCRATCH_OFF = 2048;        // after the barriers: 8 warps x 32 x 32 fp32 slow-path scratch
+constexpr int INV_SLOTS = 8;
+constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 32 x 32 fp32 slow-path scratch
 constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 32 * 32 * 4;
 }  // namespace
 
@@ -55,10 +56,10 @@ struct ScanSmem {  // placed after the tile buffers
   uint64_t tempty[NBUF];        // epilogue has read accumulator b
   uint64_t qfull;               // prompt slice landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
-  uint64_t invfull[4];          // inv_c slot l % 4 landed (cannot lap: refill needs this tile's release)
+  uint64_t invfull[INV_SLOTS];  // inv_c slot l % 8 landed (cannot lap, see the epilogue)
   uint32_t tmem_base;
   uint32_t pad_[3];
-  float invc[4][TN];            // inverse cache-row norms of tile l in slot l % 4 (bulk-copied with box 0)
+  float invc[INV_SLOTS][TN];    // inverse cache-row norms of tile l in slot l % 8 (bulk copy)
 };
 
 // Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 32 * EPI_WARPS);
     }
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
-    for (int s = 0; s < 4; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
+    for (int s = 0; s < INV_SLOTS; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
     tc::mbar_init(tc::smem_u32(&sm->qready), 32 * EPI_WARPS);
     tc::fence_barrier_init();
   }
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_arrive_expect_tx(fb, (uint32_t)(KB * BOX_BYTES));
         for (int kb = 0; kb < KB; ++kb) {
           if (kb == 0) {  // the tile's inverse norms (rows past capacity read zeros)
-            const uint32_t ib = tc::smem_u32(&sm->invfull[l & 3]);
+            const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
             tc::mbar_arrive_expect_tx(ib, TN * 4);
-            tc::bulk_load(tc::smem_u32(&sm->invc[l & 3][0]), a.inv_c + t * TN, TN * 4, ib);
+            tc::bulk_load(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib);
           }
           tc::tma_load_2d(tc::smem_u32(buf + (size_t)kb * BOX_BYTES), &tmap_c, fb, kb * KBLK, (int32_t)(t * TN));
         }
@@ -232,21 +233,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
       tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
-      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & 3]), (uint32_t)((l >> 2) & 1));
+      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       tc::fence_after();
       uint32_t v[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + h * 32, v);
       tc::tmem_wait_ld();
+      // Release accumulator b right away so MMA(l+2) never waits for this tile's
+      // processing.  inv_c slot l % 8 stays valid: the producer refills it for tile
+      // l+8 only after done(l+6), which needs every epilogue warp's release of tile
+      // l+4, which each warp gives only after finishing tile l (program order).
+      tc::fence_before();
+      tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
       if (__any_sync(0xffffffffu, active)) {
-        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & 3][h * 32]);
+        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
       }
-      // release accumulator b (and, transitively, inv_c slot l % 4) only after processing:
-      // MMA(l+2) waits for it, and the producer refills slot l % 4 only after done(l+2).
-      tc::fence_before();
-      tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
     }
     if (active) {
       uint64_t* out = a.partial + ((int64_t)(range * 2 + h) * a.N + p) * a.k;

@@ -52,7 +52,9 @@ struct MlpArgs {
   const void* W1xF;          // W1x bf16 in mma.sync B-fragment order (see k_prep_w1_frag)
   const float* W1sT;         // [k][H]
   const float* b1;           // [H]
-  const float* W2T;          // [H][L]
+  const float* W2;           // [L][H]
+  float* hbuf;               // [ceil(N/16)*16][H] hidden activations (scratch)
+  int32_t* block_cnt;        // [ceil(max_batch/16)] zeroed tickets (last-CTA election)
   const float* b2;           // [L]
   const int32_t* kskip;      // [L]
   const float* pth;          // [L]
@@ -60,7 +62,7 @@ struct MlpArgs {
   float delta;
   int32_t N, d, k, H, L;
   float* rhat;               // [N][L]
-  uint8_t* pref;             // [N][L] (0xFF past |A_i|)
+  uint8_t* rankof;           // [N][L] position of option v in pi_i (0xFF: not admissible)
   uint8_t* ccount;           // [N] |C_i|
   uint32_t* cmask;           // [N] compliance mask
   uint8_t* status;           // [N] base status bits (GATED_ALL)
@@ -72,7 +74,7 @@ size_t mlp_smem_bytes(int d, int k, int H, int L);
 void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
 
 struct AssignArgs {
-  const uint8_t* pref;
+  const uint8_t* rankof;     // [N][L] position of option v in pi_i (0xFF: not admissible)
   const uint8_t* ccount;
   const uint32_t* cmask;
   int32_t quota[32];         // [L] per-option quotas c_v (by value)

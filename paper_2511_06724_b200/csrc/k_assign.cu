@@ -135,12 +135,13 @@ __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
 }
 
 void launch_assign(const AssignArgs& a, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  const size_t smem = assign_smem_bytes(a.N > 0 ? a.N : 1, a.L);
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
   }
-  k_assign<<<1, ASSIGN_THREADS, assign_smem_bytes(a.N > 0 ? a.N : 1, a.L), s>>>(a);
+  k_assign<<<1, ASSIGN_THREADS, smem, s>>>(a);
 }
 
 }  // namespace argus

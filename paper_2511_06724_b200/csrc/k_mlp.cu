@@ -209,10 +209,10 @@ size_t mlp_smem_bytes(int d, int k, int H, int L) {
 
 void launch_mlp(const MlpArgs& a, cudaStream_t s) {
   const size_t smem = mlp_smem_bytes(a.d, a.k, a.H, a.L);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
   }
   const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
   k_mlp<<<grid, MLP_THREADS, smem, s>>>(a);

@@ -46,8 +46,9 @@ constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int INV_SLOTS = 8;
-constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 32 x 32 fp32 slow-path scratch
-constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 32 * 32 * 4;
+constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 16 x 32 fp32 slow-path scratch
+constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 }  // namespace
 
 struct ScanSmem {  // placed after the tile buffers
@@ -90,18 +91,22 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, 
   }
   const bool cand = __fmul_rn(m, iq) >= thr;
   if (__any_sync(0xffffffffu, cand)) {
-    if (cand) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) scratch[c * 32 + lane] = __uint_as_float(v[c]);
-      for (int c = 0; c < cmax; ++c) {
-        const float s = __fmul_rn(scratch[c * 32 + lane], iq);
-        if (s >= thr) {
-          tl.insert(pack_key(s, g0 + (uint32_t)c * world));
-          if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+    for (int half = 0; half < 2; ++half) {   // 16 columns at a time: 2 KB of scratch per warp
+      if (cand) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) scratch[c * 32 + lane] = __uint_as_float(v[half * 16 + c]);
+        const int lim = cmax - half * 16 < 16 ? cmax - half * 16 : 16;
+        for (int c = 0; c < lim; ++c) {
+          const float s = __fmul_rn(scratch[c * 32 + lane], iq);
+          if (s >= thr) {
+            tl.insert(pack_key(s, g0 + (uint32_t)(half * 16 + c) * world));
+            if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+          }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + (warp - 4) * 1024;
+    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + (warp - 4) * 512;
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path

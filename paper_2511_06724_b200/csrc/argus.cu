@@ -444,7 +444,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_idx, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_rhat, (size_t)c.max_batch * L));
-  TRY_RC(dalloc(r, &r->d_pref, (size_t)c.max_batch * L));
+  TRY_RC(dalloc(r, &r->d_pref, (size_t)c.max_batch * ((L + 3) / 4 * 4)));
   TRY_RC(dalloc(r, &r->d_ccount, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_cmask, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_status, (size_t)c.max_batch));
@@ -720,6 +720,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G,
   m.L = L;
   m.rhat = quality_dev ? quality_dev : r->d_rhat;
   m.rankof = r->d_pref;
+  m.Lw = (L + 3) / 4 * 4;
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
   uint8_t* status = status_dev ? status_dev : r->d_status;

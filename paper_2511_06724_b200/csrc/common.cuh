@@ -9,6 +9,13 @@
 
 namespace argus {
 
+// Programmatic dependent launch (PDL): every per-batch kernel is launched with
+// programmatic stream serialization, waits for its predecessor's memory with
+// griddepcontrol.wait before touching shared buffers, and lets its successor be
+// scheduled (griddepcontrol.launch_dependents) once its own main work is issued.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Monotone map fp32 -> u32 (a < b  <=>  ord(a) < ord(b) for non-NaN a, b).
 __device__ __forceinline__ uint32_t ord_f32(float s) {
   uint32_t u = __float_as_uint(s);

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
   __shared__ int32_t tot[NB];
   __shared__ int32_t wcnt[AW][NB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();
 
   // ---- stable counting sort of prompts by |C_i|
   if (tid < NB) base[tid] = 0;
@@ -91,19 +92,35 @@ __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
   bool any_overflow = false;
   for (int c0 = 0; c0 < N; c0 += CH) {
     const int n = min(CH, N - c0);
-    for (int x = tid; x < n * (Lw / 4); x += ASSIGN_THREADS) {
-      const int t = x / (Lw / 4), w = x - t * (Lw / 4);
-      const int i = order_s[c0 + t];
-      uint32_t word = 0;
+    // gather rows in priority order; 4 rows per thread in flight (the loads are independent)
+    const int W = Lw / 4;
+    const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.rankof);
+    for (int t0 = tid; t0 < n; t0 += 4 * ASSIGN_THREADS) {
+      int ii[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int v = w * 4 + e;
-        const uint32_t rk = v < L ? a.rankof[(int64_t)i * L + v] : 0xFFu;
-        word |= rk << (8 * e);
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * ASSIGN_THREADS;
+        ii[u] = t < n ? order_s[c0 + t] : -1;
       }
-      reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = word;
+      uint32_t cm[4];
+      uint32_t wd[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cm[u] = ii[u] >= 0 ? __ldg(a.cmask + ii[u]) : 0u;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) wd[u][w] = (ii[u] >= 0 && w < W) ? __ldg(rk32 + (int64_t)ii[u] * W + w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * ASSIGN_THREADS;
+        if (t < n) {
+          cm_s[t] = cm[u];
+#pragma unroll
+          for (int w = 0; w < 8; ++w)
+            if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = wd[u][w];
+        }
+      }
     }
-    for (int t = tid; t < n; t += ASSIGN_THREADS) cm_s[t] = a.cmask[order_s[c0 + t]];
     __syncthreads();
     if (warp == 0) {
       uint32_t nxt = lane < L ? rk_s[lane] : 0xFFu;
@@ -132,6 +149,7 @@ __global__ void __launch_bounds__(ASSIGN_THREADS) k_assign(AssignArgs a) {
     __syncthreads();
   }
   if (tid == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
+  pdl_launch();
 }
 
 void launch_assign(const AssignArgs& a, cudaStream_t s) {
@@ -141,7 +159,7 @@ void launch_assign(const AssignArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = smem;
   }
-  k_assign<<<1, ASSIGN_THREADS, smem, s>>>(a);
+  launch_pdl(k_assign, dim3(1), dim3(ASSIGN_THREADS), smem, s, a);
 }
 
 }  // namespace argus

@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_topk(const uint64_t*
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ uint64_t wl[MERGE_WARPS][KMAX];
+  pdl_wait();
   TopList<KMAX> l;
   l.clear();
   const int total = P * k;
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_topk(const uint64_t*
   }
   warp_merge_topk<KMAX>(l, k, wl[warp]);
   __syncthreads();
+  pdl_launch();
   if (warp == 0) {
     TopList<KMAX> m;
     m.clear();
@@ -64,9 +66,9 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_topk(const uint64_t*
 void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint64_t* keys_out,
                        uint32_t* idx_out, float* score_out, cudaStream_t s) {
   if (k <= 4)
-    k_merge_topk<4><<<N, MERGE_WARPS * 32, 0, s>>>(in, P, N, k, keys_out, idx_out, score_out);
+    launch_pdl(k_merge_topk<4>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, keys_out, idx_out, score_out);
   else
-    k_merge_topk<8><<<N, MERGE_WARPS * 32, 0, s>>>(in, P, N, k, keys_out, idx_out, score_out);
+    launch_pdl(k_merge_topk<8>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, keys_out, idx_out, score_out);
 }
 
 }  // namespace argus

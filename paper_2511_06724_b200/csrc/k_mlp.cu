@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
   const int i0 = pb * PB;
   const int nP = min(PB, a.N - i0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
 
   for (int idx = tid; idx < PB * (d / 8); idx += MLP_THREADS) {
     const int p = idx / (d / 8), c = idx - p * (d / 8);
@@ -110,11 +111,14 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
     is_last = ticket == (int)gridDim.y - 1;
   }
   __syncthreads();
+  pdl_launch();
   if (!is_last) return;
   __threadfence();
   if (tid == 0) a.block_cnt[pb] = 0;  // ready for the next launch
   float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]  (reuses the staging area)
+  float* w2s = hs + PB * H;                     // [L][H]
   for (int e = tid; e < PB * H; e += MLP_THREADS) hs[e] = __ldcg(a.hbuf + (int64_t)i0 * H + e);
+  for (int e = tid; e < L * H; e += MLP_THREADS) w2s[e] = __ldg(a.W2 + e);
   __syncthreads();
 
   for (int p = warp; p < nP; p += MLP_WARPS) {
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
       const float hj = hs[p * H + j];
 #pragma unroll
       for (int v = 0; v < 32; ++v)
-        if (v < L) part[v] = __fmaf_rn(__ldg(a.W2 + (int64_t)v * H + j), hj, part[v]);
+        if (v < L) part[v] = __fmaf_rn(w2s[v * H + j], hj, part[v]);
     }
     float z = 0.f;
 #pragma unroll
@@ -167,7 +171,9 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
     }
     if (act) {
       a.rhat[(int64_t)i * L + lane] = r;
-      a.rankof[(int64_t)i * L + lane] = adm ? (uint8_t)rank : (uint8_t)0xFF;  // position of v in pi_i
+      a.rankof[(int64_t)i * a.Lw + lane] = adm ? (uint8_t)rank : (uint8_t)0xFF;  // position of v in pi_i
+    } else if (lane < a.Lw) {
+      a.rankof[(int64_t)i * a.Lw + lane] = 0xFF;
     }
     if (lane == 0) {
       a.ccount[i] = (uint8_t)__popc(cmask);
@@ -201,9 +207,8 @@ void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStr
 }
 
 size_t mlp_smem_bytes(int d, int k, int H, int L) {
-  (void)L;
   const size_t phase1 = (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)MLP_WARPS * PB * 32 + (size_t)PB * k);
-  const size_t phase2 = sizeof(float) * (size_t)PB * H;
+  const size_t phase2 = sizeof(float) * ((size_t)PB * H + (size_t)L * H);
   return phase1 > phase2 ? phase1 : phase2;
 }
 
@@ -215,7 +220,7 @@ void launch_mlp(const MlpArgs& a, cudaStream_t s) {
     attr_set = smem;
   }
   const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
-  k_mlp<<<grid, MLP_THREADS, smem, s>>>(a);
+  launch_pdl(k_mlp, grid, dim3(MLP_THREADS), smem, s, a);
 }
 
 }  // namespace argus

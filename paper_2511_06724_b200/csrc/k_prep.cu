@@ -55,6 +55,7 @@ __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, in
                                uint32_t* flags) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_wait();  // the previous batch's kernels may still read Xb / inv_q
   if (warp >= n_pad) return;
   if (warp >= N) {  // zero padding rows: score 0, never reported
     uint32_t* z = reinterpret_cast<uint32_t*>(Xb + (int64_t)warp * d);
@@ -69,6 +70,7 @@ __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, in
     inv_q[warp] = bad ? 0.f : __fdiv_rn(1.0f, __fsqrt_rn(ss));
     if (bad) atomicOr(flags, FLAG_INVALID_INPUT);
   }
+  pdl_launch();
 }
 
 void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank,
@@ -86,7 +88,7 @@ void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __
                          float* inv_q, uint32_t* flags, cudaStream_t s) {
   const int threads = 256;
   int blocks = (n_pad * 32 + threads - 1) / threads;
-  k_prep_queries<<<blocks, threads, 0, s>>>(X, N, n_pad, d, Xb, inv_q, flags);
+  launch_pdl(k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, flags);
 }
 
 }  // namespace argus

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = sm->tmem_base;
+  pdl_wait();  // setup above overlapped the previous kernel; Xb / inv_q / partial are shared
 
   if (warp == 0) {
     // ======================= TMA producer
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   tc::fence_before();
   __syncthreads();
+  pdl_launch();
   if (warp == 2) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
@@ -295,9 +297,9 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
   }
   const dim3 grid(slices * ranges);
   if (a.k <= 4)
-    k_scan_tc<4><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, *tmap_q, a, slices, ranges, n_tiles);
+    launch_pdl(k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, ranges, n_tiles);
   else
-    k_scan_tc<8><<<grid, THREADS, SMEM_BYTES, s>>>(*tmap, *tmap_q, a, slices, ranges, n_tiles);
+    launch_pdl(k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, ranges, n_tiles);
 }
 
 }  // namespace argus

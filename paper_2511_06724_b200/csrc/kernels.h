@@ -2,10 +2,28 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
 namespace argus {
+
+// Launch with programmatic stream serialization (PDL); see common.cuh.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // error flags written by kernels into a device word (bitwise OR)
 enum : uint32_t { FLAG_INVALID_INPUT = 1u, FLAG_OVERFLOW = 2u };
@@ -62,7 +80,8 @@ struct MlpArgs {
   float delta;
   int32_t N, d, k, H, L;
   float* rhat;               // [N][L]
-  uint8_t* rankof;           // [N][L] position of option v in pi_i (0xFF: not admissible)
+  uint8_t* rankof;           // [N][Lw] position of option v in pi_i (0xFF: not admissible)
+  int32_t Lw;                // row stride of rankof: L rounded up to 4
   uint8_t* ccount;           // [N] |C_i|
   uint32_t* cmask;           // [N] compliance mask
   uint8_t* status;           // [N] base status bits (GATED_ALL)
@@ -74,7 +93,7 @@ size_t mlp_smem_bytes(int d, int k, int H, int L);
 void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
 
 struct AssignArgs {
-  const uint8_t* rankof;     // [N][L] position of option v in pi_i (0xFF: not admissible)
+  const uint8_t* rankof;     // [N][Lw] position of option v in pi_i (0xFF: not admissible)
   const uint8_t* ccount;
   const uint32_t* cmask;
   int32_t quota[32];         // [L] per-option quotas c_v (by value)

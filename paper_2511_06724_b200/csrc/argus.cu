@@ -114,8 +114,12 @@ struct argus_router {
   uint8_t* d_status = nullptr;     // [max_batch]
   int32_t* d_option = nullptr;     // [max_batch]
   int32_t* d_order = nullptr;      // [max_batch]
-  uint32_t* d_flags = nullptr;     // error / overflow flags
-  uint32_t* h_flags = nullptr;     // pinned mirror
+  uint32_t* d_flags = nullptr;     // error / overflow flags (first word of d_outblk)
+  uint32_t* h_flags = nullptr;     // pinned mirror of the flags word
+  uint8_t* d_outblk = nullptr;     // host-path outputs, packed after the flags word (one D2H per batch)
+  uint8_t* h_outblk = nullptr;     // pinned mirror
+  size_t outblk_bytes = 0;
+  bool pending = false;            // async (_dev) work enqueued since the last argus_sync
   CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
   CUtensorMap tmap_q;              // TMA descriptor of the bf16 prompt batch (64x128 boxes, SW128)
   bool scan_simt = false;          // debug cross-check path (ARGUS_SCAN_SIMT=1)
@@ -347,10 +351,12 @@ int argus_route_destroy(argus_router* r) {
                   r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
-                  r->d_order, r->d_flags};
+                  r->d_order};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
+  if (r->h_outblk) cudaFreeHost(r->h_outblk);
+  if (r->d_outblk) cudaFree(r->d_outblk);
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->comm) nccl().CommDestroy(r->comm);
@@ -450,7 +456,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_status, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_option, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_order, (size_t)c.max_batch));
-  TRY_RC(dalloc(r, &r->d_flags, 1));
+  r->outblk_bytes = 16 + 16 * 5 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1);
+  TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
+  r->d_flags = reinterpret_cast<uint32_t*>(r->d_outblk);
+  if (cudaMallocHost((void**)&r->h_outblk, r->outblk_bytes) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (!make_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d, 64) ||
       !make_tmap(&r->tmap_q, r->d_Xb, r->n_pad_max, d, 128)) {
@@ -760,6 +769,7 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     return ARGUS_E_INVALID;
   for (int v = 0; v < r->cfg.L; ++v)
     if (quota[v] < 0) return ARGUS_E_INVALID;
+  r->pending = true;
   if (!nccl_mode(r)) {  // single shard: the local merge is final and decodes ids / scores directly
     rc = partial_impl(r, prompts_dev, N, r->d_keys, topk_idx_dev, topk_score_dev);
     if (rc) return rc;
@@ -781,6 +791,7 @@ int argus_sync(argus_router* r) {
   CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
   CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
   CU_TRY(r, cudaStreamSynchronize(r->stream));
+  r->pending = false;
   const uint32_t fl = *r->h_flags;
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
@@ -798,21 +809,38 @@ int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const in
   if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
-  rc = argus_sync(r);  // drain earlier async work and clear its deferred flags
-  if (rc < 0) return rc;
+  if (r->pending) {  // drain earlier async work and clear its deferred flags
+    rc = argus_sync(r);
+    if (rc < 0) return rc;
+  }
+  for (int v = 0; v < L; ++v)
+    if (quota[v] < 0) return ARGUS_E_INVALID;
+  // packed output block for this N: [flags | option | idx | score | rhat | status]
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_opt = 16, o_idx = al(o_opt + 4 * (size_t)N), o_sc = al(o_idx + 4 * (size_t)N * k),
+               o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L), o_end = o_st + N;
+  uint8_t* D = r->d_outblk;
   if (root)
     CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, prompts, sizeof(float) * N * d, cudaMemcpyHostToDevice, r->stream));
-  rc = argus_route_batch_dev(r, r->d_Xstage, N, quota, r->d_option, r->d_idx, r->d_score, r->d_rhat,
-                             r->d_status);
+  rc = argus_route_batch_dev(r, r->d_Xstage, N, quota, reinterpret_cast<int32_t*>(D + o_opt),
+                             reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
+                             reinterpret_cast<float*>(D + o_rh), D + o_st);
   if (rc) return rc;
-  CU_TRY(r, cudaMemcpyAsync(option_out, r->d_option, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, r->stream));
-  CU_TRY(r, cudaMemcpyAsync(topk_idx, r->d_idx, sizeof(uint32_t) * N * k, cudaMemcpyDeviceToHost, r->stream));
-  CU_TRY(r, cudaMemcpyAsync(topk_score, r->d_score, sizeof(float) * N * k, cudaMemcpyDeviceToHost, r->stream));
-  if (quality_out)
-    CU_TRY(r, cudaMemcpyAsync(quality_out, r->d_rhat, sizeof(float) * N * L, cudaMemcpyDeviceToHost, r->stream));
-  if (status_out)
-    CU_TRY(r, cudaMemcpyAsync(status_out, r->d_status, N, cudaMemcpyDeviceToHost, r->stream));
-  return argus_sync(r);
+  CU_TRY(r, cudaMemcpyAsync(r->h_outblk, D, o_end, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));
+  r->pending = false;
+  const uint8_t* H = r->h_outblk;
+  memcpy(option_out, H + o_opt, 4 * (size_t)N);
+  memcpy(topk_idx, H + o_idx, 4 * (size_t)N * k);
+  memcpy(topk_score, H + o_sc, 4 * (size_t)N * k);
+  if (quality_out) memcpy(quality_out, H + o_rh, 4 * (size_t)N * L);
+  if (status_out) memcpy(status_out, H + o_st, (size_t)N);
+  uint32_t fl;
+  memcpy(&fl, H, 4);
+  if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
+  if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
+  return ARGUS_OK;
 }
 
 }  // extern "C"

@@ -16,6 +16,15 @@ namespace argus {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// 16-byte asynchronous global -> shared copy (LDGSTS): many in flight per thread,
+// no register round trip; cp_async_wait_all() before __syncthreads().
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Monotone map fp32 -> u32 (a < b  <=>  ord(a) < ord(b) for non-NaN a, b).
 __device__ __forceinline__ uint32_t ord_f32(float s) {
   uint32_t u = __float_as_uint(s);

@@ -49,16 +49,25 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_wait();
 
+  // stage the prompt block (rows past N in Xb are zero padding) with async copies
   for (int idx = tid; idx < PB * (d / 8); idx += MLP_THREADS) {
     const int p = idx / (d / 8), c = idx - p * (d / 8);
-    uint4 u = make_uint4(0, 0, 0, 0);
-    if (p < nP) u = reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d)[c];
-    *reinterpret_cast<uint4*>(xs + p * RS + c * 8) = u;
+    cp_async16(xs + p * RS + c * 8, reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d) + c);
   }
   for (int idx = tid; idx < PB * k; idx += MLP_THREADS) {
     const int p = idx / k;
     ss[idx] = p < nP ? a.topk_score[(int64_t)(i0 + p) * k + (idx - p * k)] : 0.f;
   }
+  // per-thread epilogue constants of layer 1 (independent of the staging above)
+  float w1s_r[2][8], b1_r[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int j = cc * 32 + ((tid + u * MLP_THREADS) & 31);
+    b1_r[u] = __ldg(a.b1 + j);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
+  }
+  cp_async_wait_all();
   __syncthreads();
 
   // ---- layer 1, hidden units [32 cc, 32 cc + 32), warp w takes a 1/8 slice of d
@@ -95,13 +104,17 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
   }
   __syncthreads();
   // reduce the 8 split-K partials (fixed order), + W1s . s + b1, relu -> h (global)
-  for (int e = tid; e < PB * 32; e += MLP_THREADS) {
-    const int row = e >> 5, jl = e & 31, j = cc * 32 + jl;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {  // PB * 32 = 2 * MLP_THREADS elements
+    const int e = tid + u * MLP_THREADS;
+    const int row = e >> 5, j = cc * 32 + (e & 31);
     float z = 0.f;
 #pragma unroll
     for (int w = 0; w < MLP_WARPS; ++w) z = __fadd_rn(z, red[w * PB * 32 + e]);
-    for (int q = 0; q < k; ++q) z = __fmaf_rn(a.W1sT[q * H + j], ss[row * k + q], z);
-    a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, a.b1[j]), 0.f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < k) z = __fmaf_rn(w1s_r[u][q], ss[row * k + q], z);
+    a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, b1_r[u]), 0.f);
   }
   // ---- the last CTA of this prompt block runs layer 2 + A5
   __threadfence();
@@ -117,8 +130,10 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
   if (tid == 0) a.block_cnt[pb] = 0;  // ready for the next launch
   float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]  (reuses the staging area)
   float* w2s = hs + PB * H;                     // [L][H]
-  for (int e = tid; e < PB * H; e += MLP_THREADS) hs[e] = __ldcg(a.hbuf + (int64_t)i0 * H + e);
-  for (int e = tid; e < L * H; e += MLP_THREADS) w2s[e] = __ldg(a.W2 + e);
+  // cp.async.cg reads through L2 only (hbuf was written by other CTAs of this launch)
+  for (int e = tid; e < PB * H / 4; e += MLP_THREADS) cp_async16(hs + 4 * e, a.hbuf + (int64_t)i0 * H + 4 * e);
+  for (int e = tid; e < L * H / 4; e += MLP_THREADS) cp_async16(w2s + 4 * e, a.W2 + 4 * e);
+  cp_async_wait_all();
   __syncthreads();
 
   for (int p = warp; p < nP; p += MLP_WARPS) {

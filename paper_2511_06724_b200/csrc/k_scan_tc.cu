@@ -257,8 +257,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
       }
     }
-    if (active) {
-      uint64_t* out = a.partial + ((int64_t)(range * 2 + h) * a.N + p) * a.k;
+    // fold the two column halves of each prompt inside the CTA: half 1 parks its list
+    // in the (now idle) tile buffers, half 0 merges and writes one list per range
+    uint64_t* xchg = reinterpret_cast<uint64_t*>(ring) + (size_t)(q * 32 + lane) * KMAX;
+    if (h == 1) {
+#pragma unroll
+      for (int t2 = 0; t2 < KMAX; ++t2) xchg[t2] = tl.v[t2];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+    if (h == 0 && active) {
+#pragma unroll
+      for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(xchg[t2]);
+      uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2)
         if (t2 < a.k) out[t2] = tl.v[t2];
@@ -280,14 +290,14 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
   if (ranges < 1) ranges = 1;
   const int64_t n_tiles = (m_local + TN - 1) / TN;
   if (ranges > n_tiles) ranges = (int)(n_tiles > 0 ? n_tiles : 1);
-  return 2 * ranges;  // partial lists: one per (range, column half)
+  return ranges;  // one partial list per (range, prompt)
 }
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s) {
   const int slices = (a.N + TM - 1) / TM;
-  const int ranges = a.P / 2;
+  const int ranges = a.P;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   static bool attr = false;
   if (!attr) {

@@ -178,11 +178,8 @@ def main():
     sizes = batch_sizes(cfg) if not args.fixed_n else [args.fixed_n] * N_TRACE
     max_batch = max(max(sizes), max([int(x) for x in args.sweep.split(",") if x] or [0]))
 
-    uid = None
-    if world > 1:
-        obj = [argus.argus_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+    from paper_2511_06724_b200 import dist as adist
+    uid = adist.share_nccl_id(dist, rank, argus.argus_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.Stream()
     r = argus.Router(d, k, opts, W1, b1, W2, b2, capacity=cfg.M, max_batch=max_batch, rank=rank, world=world,
                      device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream)
@@ -240,11 +237,7 @@ def main():
     launches = r.argus_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     barrier()
-    ms_max = ms
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_max = float(tt.item())
+    ms_max = adist.max_over_ranks(dist, ms, dev) if world > 1 else ms
     # per-kernel CUDA-event timing over the same K steps in a second pass (event
     # records between kernels would break the programmatic-dependent-launch overlap
     # of the timed pass above)
@@ -278,9 +271,7 @@ def main():
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        e2e_ms = adist.max_over_ranks(dist, e2e_ms, dev)
 
     if args.sweep:
         sweep(args, r, cg, cache_rows, cfg, fr, out, stream, argus)
@@ -288,7 +279,7 @@ def main():
     # ---- roofline of the dominant kernel (the scan)
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
     scan_ms, scan_n = prof["scan"]
-    m_local = (cfg.M + world - 1) // world
+    m_local = adist.local_rows(cfg.M, world, 0)
     bytes_per_launch = m_local * (2 * d + 4)
     achieved_gbs = bytes_per_launch * scan_n / (scan_ms / 1e3) / 1e9 if scan_n else None
     flops = sum(2.0 * sizes[t % N_TRACE] * m_local * d for t in range(args.warmup, args.warmup + args.steps))

@@ -1,0 +1,40 @@
+"""Host-side multi-GPU plumbing around libargus (one process per GPU).
+
+The data path (scan, merge, predictor, assignment, NCCL broadcast/all-gather)
+lives in libargus.so; this module only holds the host protocol that callers and
+bench.py share: the striped cache layout (global id g on rank g mod G at slot
+g div G), distribution of the NCCL unique id over the caller's
+process group, and max-over-ranks timing.  Tested with world_size=2 gloo on CPU
+(tests/test_multi_gloo.py).
+"""
+from __future__ import annotations
+
+
+def stripe_owner(g: int, world: int) -> int:
+    """Rank holding global cache id g."""
+    return g % world
+
+
+def stripe_slot(g: int, world: int) -> int:
+    """Local row of global id g on its owner."""
+    return g // world
+
+
+def local_rows(M: int, world: int, rank: int) -> int:
+    """Rows of an M-entry cache held by `rank` (shards differ by at most one)."""
+    return (M + world - 1 - rank) // world
+
+
+def share_nccl_id(dist, rank: int, make_id):
+    """Rank 0 creates the 128-byte ncclUniqueId, every rank returns the same bytes."""
+    obj = [make_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(dist, value: float, device=None) -> float:
+    """Max of a per-rank float (elapsed ms) over the group: the job's time."""
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -84,3 +84,18 @@ def test_init_rejects_bad_config_without_touching_gpu(argus):
     W1[3, 7] = np.inf
     with pytest.raises(argus.ArgusError):
         argus.Router(768, 4, p.opts, W1, p.b1, p.W2, p.b2, 10, 4)
+
+
+def test_product_never_imports_oracle():
+    """The CUDA path shares no code with the oracle and never loads it."""
+    pkg = os.path.join(ROOT, "paper_2511_06724_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "argus_oracle" not in src and "liboracle" not in src, f
+    lib = os.path.join(pkg, "libargus.so")
+    if os.path.exists(lib):
+        out = subprocess.run(["ldd", lib], capture_output=True, text=True).stdout
+        assert "oracle" not in out

@@ -39,22 +39,25 @@ constexpr int TM = 128;                     // prompts per CTA (UMMA M)
 constexpr int KBLK = 64;                    // bf16 per 128-byte swizzle row
 constexpr int KB_MAX = 12;                  // d <= 768
 constexpr int BOX_BYTES = TN * KBLK * 2;    // 8 KB cache box
-constexpr int TILE_BYTES = KB_MAX * BOX_BYTES;  // 96 KB tile buffer
-constexpr int NBUF = 2;
+constexpr int HALF_BOXES = KB_MAX / 2;      // a tile streams through two half-tile slots
+constexpr int SLOT_BYTES = HALF_BOXES * BOX_BYTES;  // 48 KB
+constexpr int NSLOT = 4;                    // ring of half-tile slots (2 tiles)
+constexpr int RING_BYTES = NSLOT * SLOT_BYTES;      // 192 KB (also holds the 128 x d prompt slice at start)
 constexpr int THREADS = 384;               // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int INV_SLOTS = 8;
 constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 16 x 32 fp32 slow-path scratch
-constexpr size_t SMEM_BYTES = (size_t)NBUF * TILE_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
+constexpr size_t SMEM_BYTES = (size_t)RING_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 }  // namespace
 
-struct ScanSmem {  // placed after the tile buffers
-  uint64_t full[NBUF];          // all TMA boxes of the tile in buffer b landed
-  uint64_t done[NBUF];          // all MMAs of the tile in buffer b complete (one commit per tile)
-  uint64_t tempty[NBUF];        // epilogue has read accumulator b
+struct ScanSmem {  // placed after the ring
+  uint64_t full[NSLOT];         // TMA boxes of half-tile slot s landed
+  uint64_t empty[NSLOT];        // MMAs reading slot s complete (one commit per half tile); for a
+                                // tile's second half this also means the accumulator is final
+  uint64_t tempty[2];           // epilogue has read accumulator b
   uint64_t qfull;               // prompt slice landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
   uint64_t invfull[INV_SLOTS];  // inv_c slot l % 8 landed (cannot lap, see the epilogue)
@@ -71,14 +74,13 @@ struct ScanSmem {  // placed after the tile buffers
 // memory (column-major, conflict-free) and each lane rescans its own 32 with the
 // exact score s = fl(x * inv_q) and inserts into its register top-k.
 template <int KMAX>
-__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, float iq, int cmax, uint32_t g0,
-                                          uint32_t world, TopList<KMAX>& tl, float& thr,
-                                          float* __restrict__ scratch) {
+__device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float iq, int cmax, uint32_t g0,
+                                          uint32_t world, TopList<KMAX>& tl, float& thr, uint32_t scratch) {
   const int lane = threadIdx.x & 31;
   float m = -INFINITY;
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
-    const float4 ic = icp[c4];   // shared memory, same address in every lane (broadcast)
+    const float4 ic = tc::lds_f32x4(icp + c4 * 16);   // shared memory, same address in every lane (broadcast)
     const float x0 = __fmul_rn(__uint_as_float(v[c4 * 4 + 0]), ic.x);
     const float x1 = __fmul_rn(__uint_as_float(v[c4 * 4 + 1]), ic.y);
     const float x2 = __fmul_rn(__uint_as_float(v[c4 * 4 + 2]), ic.z);
@@ -95,10 +97,10 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], const float4* icp, 
     for (int half = 0; half < 2; ++half) {   // 16 columns at a time: 2 KB of scratch per warp
       if (cand) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) scratch[c * 32 + lane] = __uint_as_float(v[half * 16 + c]);
+        for (int c = 0; c < 16; ++c) tc::sts_f32(scratch + (uint32_t)(c * 32 + lane) * 4, __uint_as_float(v[half * 16 + c]));
         const int lim = cmax - half * 16 < 16 ? cmax - half * 16 : 16;
         for (int c = 0; c < lim; ++c) {
-          const float s = __fmul_rn(scratch[c * 32 + lane], iq);
+          const float s = __fmul_rn(tc::lds_f32(scratch + (uint32_t)(c * 32 + lane) * 4), iq);
           if (s >= thr) {
             tl.insert(pack_key(s, g0 + (uint32_t)(half * 16 + c) * world));
             if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
@@ -116,7 +118,8 @@ __global__ void __launch_bounds__(THREADS, 1)
               int slices, int ranges, int64_t n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)NBUF * TILE_BYTES);
+  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)RING_BYTES);
+  const uint32_t ring_s = tc::smem_u32(ring);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x % slices;
   const int range = blockIdx.x / slices;
@@ -127,11 +130,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmap_c);
     tc::prefetch_tmap(&tmap_q);
-    for (int b = 0; b < NBUF; ++b) {
-      tc::mbar_init(tc::smem_u32(&sm->full[b]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->done[b]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 32 * EPI_WARPS);
+    for (int s = 0; s < NSLOT; ++s) {
+      tc::mbar_init(tc::smem_u32(&sm->full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&sm->empty[s]), 1);
     }
+    for (int b = 0; b < 2; ++b) tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 32 * EPI_WARPS);
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
     for (int s = 0; s < INV_SLOTS; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
     tc::mbar_init(tc::smem_u32(&sm->qready), 32 * EPI_WARPS);
@@ -154,22 +157,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t qb = tc::smem_u32(&sm->qfull);
       tc::mbar_arrive_expect_tx(qb, (uint32_t)(KB * TM * KBLK * 2));
       for (int kb = 0; kb < KB; ++kb)
-        tc::tma_load_2d(tc::smem_u32(ring + (size_t)kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
-      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // buffers free again
+        tc::tma_load_2d(ring_s + (uint32_t)(kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
+      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // ring free again
+      const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int64_t l = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++l) {
-        const int b = (int)(l & 1);
-        if (l >= NBUF) tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)(((l - NBUF) >> 1) & 1));
-        uint8_t* buf = ring + (size_t)b * TILE_BYTES;
-        const uint32_t fb = tc::smem_u32(&sm->full[b]);
-        tc::mbar_arrive_expect_tx(fb, (uint32_t)(KB * BOX_BYTES));
-        for (int kb = 0; kb < KB; ++kb) {
-          if (kb == 0) {  // the tile's inverse norms (rows past capacity read zeros)
+        for (int hh = 0; hh < 2; ++hh) {
+          const int64_t u = 2 * l + hh;  // half-tile sequence number
+          const int sl = (int)(u & (NSLOT - 1));
+          tc::mbar_wait(tc::smem_u32(&sm->empty[sl]), (uint32_t)(((u >> 2) & 1) ^ 1));
+          const uint32_t fb = tc::smem_u32(&sm->full[sl]);
+          tc::mbar_arrive_expect_tx(fb, (uint32_t)(kb_half[hh] * BOX_BYTES));
+          if (hh == 0) {  // the tile's inverse norms (rows past capacity read zeros)
             const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
             tc::mbar_arrive_expect_tx(ib, TN * 4);
             tc::bulk_load(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib);
           }
-          tc::tma_load_2d(tc::smem_u32(buf + (size_t)kb * BOX_BYTES), &tmap_c, fb, kb * KBLK, (int32_t)(t * TN));
+          const int kb0 = hh ? kb_half[0] : 0;
+          for (int j = 0; j < kb_half[hh]; ++j)
+            tc::tma_load_2d(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb, (kb0 + j) * KBLK,
+                            (int32_t)(t * TN));
         }
       }
     }
@@ -179,24 +186,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
       tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
       tc::fence_after();
+      const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int64_t l = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++l) {
         const int b = (int)(l & 1);
-        const uint32_t ph = (uint32_t)((l >> 1) & 1);
-        tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), ph ^ 1);
+        tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
         tc::fence_after();
         const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
-        const uint32_t sbuf = tc::smem_u32(ring + (size_t)b * TILE_BYTES);
-        tc::mbar_wait(tc::smem_u32(&sm->full[b]), ph);
-        tc::fence_after();
-        for (int kb = 0; kb < KB; ++kb) {
-          const uint32_t sb = sbuf + kb * BOX_BYTES;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int64_t u = 2 * l + hh;
+          const int sl = (int)(u & (NSLOT - 1));
+          tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 2) & 1));
+          tc::fence_after();
+          const int kb0 = hh ? kb_half[0] : 0;
+          for (int j = 0; j < kb_half[hh]; ++j) {
+            const uint32_t sb = ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES);
+            const int kb = kb0 + j;
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk)
-            tc::mma_ts(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8), tc::desc_kmajor_sw128(sb + kk * 32),
-                       IDESC, (kb | kk) != 0);
+            for (int kk = 0; kk < KBLK / 16; ++kk)
+              tc::mma_ts(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8), tc::desc_kmajor_sw128(sb + kk * 32),
+                         IDESC, (kb | kk) != 0);
+          }
+          // frees slot sl; after the second half it also marks accumulator b final
+          tc::mma_commit(tc::smem_u32(&sm->empty[sl]));
         }
-        tc::mma_commit(tc::smem_u32(&sm->done[b]));  // frees buffer b AND hands accumulator b to the epilogue
       }
     }
   } else if (warp >= 4) {
@@ -210,11 +223,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(tc::smem_u32(&sm->qfull), 0);
       const int sw = p_local & 7;  // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r % 8)
       for (int c = h; c < KB; c += 2) {   // 64 bf16 = 32 TMEM columns per box; halves split the boxes
-        const uint8_t* row = ring + (size_t)c * TM * KBLK * 2 + (size_t)p_local * 128;
+        const uint32_t row = ring_s + (uint32_t)(c * TM * KBLK * 2 + p_local * 128);
         uint32_t r[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const uint4 u = *reinterpret_cast<const uint4*>(row + ((j ^ sw) << 4));
+          const uint4 u = tc::lds_u32x4(row + (uint32_t)((j ^ sw) << 4));
           r[4 * j + 0] = u.x;
           r[4 * j + 1] = u.y;
           r[4 * j + 2] = u.z;
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    float* scratch = reinterpret_cast<float*>(ring + (size_t)NBUF * TILE_BYTES + SCRATCH_OFF) + (warp - 4) * 512;
+    const uint32_t scratch = ring_s + (uint32_t)(RING_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
@@ -238,7 +251,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
-      tc::mbar_wait(tc::smem_u32(&sm->done[b]), (uint32_t)((l >> 1) & 1));
+      // the tile's second half-slot (2l+1) % 4 completing means all its MMAs are done;
+      // it cannot lap: reuse by tile l+2 needs this warp's release of tile l
+      tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l + 1) & (NSLOT - 1)]), (uint32_t)((l >> 1) & 1));
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       tc::fence_after();
       uint32_t v[32];
@@ -251,7 +266,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::fence_before();
       tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
       if (__any_sync(0xffffffffu, active)) {
-        const float4* icp = reinterpret_cast<const float4*>(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
+        const uint32_t icp = tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
@@ -259,15 +274,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // fold the two column halves of each prompt inside the CTA: half 1 parks its list
     // in the (now idle) tile buffers, half 0 merges and writes one list per range
-    uint64_t* xchg = reinterpret_cast<uint64_t*>(ring) + (size_t)(q * 32 + lane) * KMAX;
+    const uint32_t xchg = ring_s + (uint32_t)((q * 32 + lane) * KMAX * 8);
     if (h == 1) {
 #pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2) xchg[t2] = tl.v[t2];
+      for (int t2 = 0; t2 < KMAX; ++t2) tc::sts_u64(xchg + t2 * 8, tl.v[t2]);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
     if (h == 0 && active) {
 #pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(xchg[t2]);
+      for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(tc::lds_u64(xchg + t2 * 8));
       uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2)

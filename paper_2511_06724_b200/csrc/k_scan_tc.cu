@@ -181,35 +181,36 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
-      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
+    // ======================= MMA issuer (warp-uniform loop, elect.sync issue)
+    constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
+    tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
+    tc::fence_after();
+    const int kb_half0 = (KB + 1) / 2;
+    const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
+    int64_t l = 0;
+    for (int64_t t = t_begin; t < t_end; ++t, ++l) {
+      const int b = (int)(l & 1);
+      tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
       tc::fence_after();
-      const int kb_half[2] = {(KB + 1) / 2, KB / 2};
-      int64_t l = 0;
-      for (int64_t t = t_begin; t < t_end; ++t, ++l) {
-        const int b = (int)(l & 1);
-        tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
-        tc::fence_after();
-        const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
-        for (int hh = 0; hh < 2; ++hh) {
-          const int64_t u = 2 * l + hh;
-          const int sl = (int)(u & (NSLOT - 1));
-          tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 2) & 1));
-          tc::fence_after();
-          const int kb0 = hh ? kb_half[0] : 0;
-          for (int j = 0; j < kb_half[hh]; ++j) {
-            const uint32_t sb = ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES);
-            const int kb = kb0 + j;
+      const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
 #pragma unroll
-            for (int kk = 0; kk < KBLK / 16; ++kk)
-              tc::mma_ts(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8), tc::desc_kmajor_sw128(sb + kk * 32),
-                         IDESC, (kb | kk) != 0);
-          }
-          // frees slot sl; after the second half it also marks accumulator b final
-          tc::mma_commit(tc::smem_u32(&sm->empty[sl]));
+      for (int hh = 0; hh < 2; ++hh) {
+        const int64_t u = 2 * l + hh;
+        const int sl = (int)(u & (NSLOT - 1));
+        tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 2) & 1));
+        tc::fence_after();
+        const int kb0 = hh ? kb_half0 : 0;
+        const int nkb = hh ? KB - kb_half0 : kb_half0;
+        const uint64_t dslot = dbase + (uint64_t)((sl * SLOT_BYTES) >> 4);
+        for (int j = 0; j < nkb; ++j) {
+          const int kb = kb0 + j;
+#pragma unroll
+          for (int kk = 0; kk < KBLK / 16; ++kk)
+            tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
+                            dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
         }
+        // frees slot sl; after the second half it also marks accumulator b final
+        tc::mma_commit_warp(tc::smem_u32(&sm->empty[sl]));
       }
     }
   } else if (warp >= 4) {

@@ -243,9 +243,15 @@ def main():
     # of the timed pass above)
     r.argus_profile_read()
     r.argus_profile_enable(True)
+    prof = {}
+    per_launch = []  # (N, scan ms) of every launch, for the per-bound roofline split
     for t in range(args.warmup, args.warmup + args.steps):
-        step(t)
-    prof = r.argus_profile_read()
+        n = step(t)
+        pr = r.argus_profile_read()  # synchronises: this pass is for timing kernels, not the headline
+        for kk, (ms_, cnt) in pr.items():
+            a0 = prof.get(kk, (0.0, 0))
+            prof[kk] = (a0[0] + ms_, a0[1] + cnt)
+        per_launch.append((n, pr["scan"][0]))
     r.argus_profile_enable(False)
     barrier()
     total_prompts = prompts  # every rank routes the same prompts; the batch is the job's unit
@@ -290,6 +296,29 @@ def main():
             tj = json.load(f)
         traffic = tj.get("dram_bytes_per_launch")
     stage_ms = {kk: round(v[0] / max(1, args.steps), 5) for kk, v in prof.items() if v[1]}
+    # per-launch roofline: each scan launch is bound by max(bytes / HBM, flops / tensor)
+    split = {"hbm": [0.0, 0.0, 0], "tensor": [0.0, 0.0, 0]}  # [work, ms, launches]
+    t_roof, t_act = 0.0, 0.0
+    for n, sms in per_launch:
+        t_h = bytes_per_launch / (hbm * 1e9) * 1e3
+        fl = 2.0 * n * m_local * d
+        t_t = fl / (tf_sust * 1e12) * 1e3
+        key = "hbm" if t_h >= t_t else "tensor"
+        split[key][0] += bytes_per_launch if key == "hbm" else fl
+        split[key][1] += sms
+        split[key][2] += 1
+        t_roof += max(t_h, t_t)
+        t_act += sms
+    roof_split = {}
+    if split["hbm"][2]:
+        g = split["hbm"][0] / (split["hbm"][1] / 1e3) / 1e9
+        roof_split["hbm_bound"] = {"launches": split["hbm"][2], "achieved": round(g, 1), "unit": "GB/s",
+                                   "frac": round(g / hbm, 4)}
+    if split["tensor"][2]:
+        tf = split["tensor"][0] / (split["tensor"][1] / 1e3) / 1e12
+        roof_split["tensor_bound"] = {"launches": split["tensor"][2], "achieved": round(tf, 1), "unit": "TFLOP/s",
+                                      "peak": tf_sust, "frac": round(tf / tf_sust, 4)}
+    roof_split["roofline_time_frac"] = round(t_roof / max(t_act, 1e-12), 4)
     total_stage = sum(v[0] for v in prof.values())
 
     res = {
@@ -333,6 +362,7 @@ def main():
             "scan_share_of_step": round(scan_ms / max(total_stage, 1e-9), 4),
             "tensor_tflops_achieved": round(flops / (scan_ms / 1e3) / 1e12, 2) if scan_ms else None,
             "tensor_peak_tflops": tf_sust,
+            "by_bound": roof_split,
         },
         "stage_ms_per_step": stage_ms,
         "route_rc": rc,

@@ -31,6 +31,10 @@
 #include "kernels.h"
 #include "tc.cuh"
 
+#ifndef ARGUS_SCAN_EXP
+#define ARGUS_SCAN_EXP 0  // diagnostics only: 1 = skip epilogue math, 2 = skip MMAs (tools/scan_experiments.sh)
+#endif
+
 namespace argus {
 
 namespace {
@@ -206,8 +210,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int kb = kb0 + j;
 #pragma unroll
           for (int kk = 0; kk < KBLK / 16; ++kk)
-            tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
-                            dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
+            if (ARGUS_SCAN_EXP != 2 || (kb | kk) == 0)
+              tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
+                              dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
         }
         // frees slot sl; after the second half it also marks accumulator b final
         tc::mma_commit_warp(tc::smem_u32(&sm->empty[sl]));
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // l+4, which each warp gives only after finishing tile l (program order).
       tc::fence_before();
       tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
-      if (__any_sync(0xffffffffu, active)) {
+      if (ARGUS_SCAN_EXP != 1 && __any_sync(0xffffffffu, active)) {
         const uint32_t icp = tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;

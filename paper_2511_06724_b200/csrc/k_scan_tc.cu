@@ -99,19 +99,31 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
   if (__any_sync(0xffffffffu, cand)) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {   // 16 columns at a time: 2 KB of scratch per warp
-      if (cand) {
+      uint32_t mask = 0;
+      if (cand) {  // exact scores of this half, candidate bits (columns past the shard excluded)
 #pragma unroll
-        for (int c = 0; c < 16; ++c) tc::sts_f32(scratch + (uint32_t)(c * 32 + lane) * 4, __uint_as_float(v[half * 16 + c]));
-        const int lim = cmax - half * 16 < 16 ? cmax - half * 16 : 16;
-        for (int c = 0; c < lim; ++c) {
-          const float s = __fmul_rn(tc::lds_f32(scratch + (uint32_t)(c * 32 + lane) * 4), iq);
-          if (s >= thr) {
-            tl.insert(pack_key(s, g0 + (uint32_t)(half * 16 + c) * world));
-            if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
-          }
+        for (int c = 0; c < 16; ++c) {
+          const float sc = __fmul_rn(__uint_as_float(v[half * 16 + c]), iq);
+          mask |= (sc >= thr && half * 16 + c < cmax) ? (1u << c) : 0u;
         }
       }
-      __syncwarp();
+      if (__any_sync(0xffffffffu, mask != 0)) {
+        if (mask) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            tc::sts_f32(scratch + (uint32_t)(c * 32 + lane) * 4, __uint_as_float(v[half * 16 + c]));
+          while (mask) {  // only the candidate columns (typically one or two)
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float sc = __fmul_rn(tc::lds_f32(scratch + (uint32_t)(c * 32 + lane) * 4), iq);
+            if (sc >= thr) {
+              tl.insert(pack_key(sc, g0 + (uint32_t)(half * 16 + c) * world));
+              if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+            }
+          }
+        }
+        __syncwarp();
+      }
     }
   }
 }

@@ -77,7 +77,7 @@ def batch_sizes(cfg):
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling via NVML during the timed region."""
 
-    def __init__(self, device_index=0, period=0.02):
+    def __init__(self, device_index=0, period=0.005):
         self.samples, self.reasons = [], set()
         self.period = period
         self._stop = threading.Event()

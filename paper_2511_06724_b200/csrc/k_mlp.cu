@@ -83,18 +83,26 @@ __global__ void __launch_bounds__(MLP_THREADS) k_mlp(MlpArgs a) {
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-#pragma unroll 2
-    for (int ks = ks0; ks < ks1; ++ks) {
-      uint2 bf[4];
+    // all of this warp's B fragments first (<= 8 k-steps x 4 n-tiles): one memory round trip
+    constexpr int KSW = 8;  // k-steps per warp for d <= 1024
+    uint2 bf[KSW][4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks) * 32 + lane);
-      uint32_t af[4];
-      af[0] = x32[g * RSW + ks * 8 + t];
-      af[1] = x32[(g + 8) * RSW + ks * 8 + t];
-      af[2] = x32[g * RSW + ks * 8 + 4 + t];
-      af[3] = x32[(g + 8) * RSW + ks * 8 + 4 + t];
+    for (int q = 0; q < KSW; ++q)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) mma_bf16_16816(acc[nt], af, bf[nt]);
+      for (int nt = 0; nt < 4; ++nt)
+        bf[q][nt] = (ks0 + q < ks1) ? __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks0 + q) * 32 + lane) : make_uint2(0, 0);
+#pragma unroll
+    for (int q = 0; q < KSW; ++q) {
+      if (ks0 + q < ks1) {
+        const int ks = ks0 + q;
+        uint32_t af[4];
+        af[0] = x32[g * RSW + ks * 8 + t];
+        af[1] = x32[(g + 8) * RSW + ks * 8 + t];
+        af[2] = x32[g * RSW + ks * 8 + 4 + t];
+        af[3] = x32[(g + 8) * RSW + ks * 8 + 4 + t];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_bf16_16816(acc[nt], af, bf[q][nt]);
+      }
     }
     float* rw = red + warp * PB * 32;
 #pragma unroll

@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int kb = 0; kb < KB; ++kb)
         tc::tma_load_2d(ring_s + (uint32_t)(kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
       tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // ring free again
+      // one slice streams the cache exactly once: evict-first; with several slices the
+      // other slices of the range re-read each tile from L2 within microseconds
+      const uint64_t pol = tc::policy_evict_first();
       const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int64_t l = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++l) {
@@ -187,12 +190,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (hh == 0) {  // the tile's inverse norms (rows past capacity read zeros)
             const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
             tc::mbar_arrive_expect_tx(ib, TN * 4);
-            tc::bulk_load(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib);
+            tc::bulk_load_hint(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib, pol);
           }
           const int kb0 = hh ? kb_half[0] : 0;
           for (int j = 0; j < kb_half[hh]; ++j)
-            tc::tma_load_2d(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb, (kb0 + j) * KBLK,
-                            (int32_t)(t * TN));
+            tc::tma_load_2d_hint(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb, (kb0 + j) * KBLK,
+                                 (int32_t)(t * TN), pol);
         }
       }
     }

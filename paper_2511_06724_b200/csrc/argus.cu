@@ -102,6 +102,7 @@ struct argus_router {
   float* d_Xstage = nullptr;       // [max(max_batch, INSERT_CHUNK)][d] fp32 staging
   __nv_bfloat16* d_Xb = nullptr;   // [n_pad_max][d]
   float* d_invq = nullptr;         // [n_pad_max]
+  uint64_t* d_gthr = nullptr;      // [n_pad_max] shared per-prompt scan threshold
   uint64_t* d_partial = nullptr;   // [p_max][max_batch][k]
   uint64_t* d_keys = nullptr;      // [max_batch][k]
   uint64_t* d_keys_all = nullptr;  // [world][max_batch][k]
@@ -351,7 +352,7 @@ int argus_route_destroy(argus_router* r) {
                   r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
-                  r->d_order};
+                  r->d_order, r->d_gthr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -444,6 +445,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_Xstage, (size_t)stage_rows * d));
   TRY_RC(dalloc(r, &r->d_Xb, (size_t)r->n_pad_max * d));
   TRY_RC(dalloc(r, &r->d_invq, (size_t)r->n_pad_max));
+  TRY_RC(dalloc(r, &r->d_gthr, (size_t)r->n_pad_max));
   TRY_RC(dalloc(r, &r->d_partial, (size_t)r->p_max * c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
@@ -636,9 +638,10 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
     StageScope sc(r, ARGUS_STAGE_PREP);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_flags, r->stream);
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_gthr, r->d_flags, r->stream);
     LAUNCHED(r);
   }
+  if (!root) CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
   if (nccl_mode(r)) {
     NC_TRY(r, nccl().GroupStart());
     NC_TRY(r, nccl().Broadcast(r->d_Xb, r->d_Xb, (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
@@ -658,6 +661,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.rank = r->cfg.rank;
   a.world = r->cfg.world;
   a.partial = r->d_partial;
+  a.gthr = r->d_gthr;
   a.P = std::min(r->scan_simt ? scan_plan_ranges_simt(a.m_local, N, r->num_sms)
                               : scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
   {

@@ -118,7 +118,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
             const float sc = __fmul_rn(tc::lds_f32(scratch + (uint32_t)(c * 32 + lane) * 4), iq);
             if (sc >= thr) {
               tl.insert(pack_key(sc, g0 + (uint32_t)(half * 16 + c) * world));
-              if (tl.v[KMAX - 1] != 0) thr = key_score(tl.v[KMAX - 1]);
+              if (tl.v[KMAX - 1] != 0) thr = fmaxf(thr, key_score(tl.v[KMAX - 1]));
             }
           }
         }
@@ -267,9 +267,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
+    // Shared threshold: gthr[p] is the largest "KMAX-th best key" any list of this
+    // prompt has published (all ranges, both column halves).  A row below it cannot
+    // be in the prompt's global top-k (KMAX >= k keys beat it), so every epilogue
+    // filters with max(own, shared); lists only grow, the shared key only rises, and
+    // a stale read is merely conservative.  Exactness is unaffected.
+    uint64_t* gthr_p = a.gthr + p;
+    uint64_t published = 0;
+    uint64_t gk = active ? __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p)) : 0;
     int64_t l = 0;
     for (int64_t t = t_begin; t < t_end; ++t, ++l) {
       __syncwarp();
+      if (gk != 0) thr = fmaxf(thr, key_score(gk));
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
       // the tile's second half-slot (2l+1) % 4 completing means all its MMAs are done;
@@ -291,6 +300,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
+        if (active && tl.v[KMAX - 1] > published) {  // rare: publish an improved local bound
+          published = tl.v[KMAX - 1];
+          atomicMax(reinterpret_cast<unsigned long long*>(gthr_p), (unsigned long long)published);
+        }
+        // refresh the shared bound for the next tile (latency overlaps the barrier wait)
+        if (active) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
       }
     }
     // fold the two column halves of each prompt inside the CTA: half 1 parks its list

@@ -300,12 +300,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
-        if (active && tl.v[KMAX - 1] > published) {  // rare: publish an improved local bound
+        // publish only a local bound that beats everything seen so far (rare after warm-up)
+        if (active && tl.v[KMAX - 1] > published && tl.v[KMAX - 1] > gk) {
           published = tl.v[KMAX - 1];
           atomicMax(reinterpret_cast<unsigned long long*>(gthr_p), (unsigned long long)published);
         }
-        // refresh the shared bound for the next tile (latency overlaps the barrier wait)
-        if (active) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
+        // refresh the shared bound every 4th tile (latency overlaps the next barrier waits)
+        if (active && (l & 3) == 3) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
       }
     }
     // fold the two column halves of each prompt inside the CTA: half 1 parks its list

@@ -200,14 +200,15 @@ int argus_get_stream(const argus_router* r, void** stream_out);
  * records a CUDA event pair on its stream around every kernel it launches;
  * argus_profile_read synchronises and returns, for one stage, the summed
  * device milliseconds and the number of launches since the last read (then
- * resets that stage).  Stages: 0 prep (K6), 1 scan (K1+K2), 2 merge over CTA
- * ranges (K5), 3 merge over shards (K5), 4 predictor (K3+A5), 5 assignment (K4),
- * 6 insert (K0). */
+ * resets that stage).  Stages: 0 prep (K6), 1 scan (K1+K2), 2 local merge before
+ * the all-gather (K5, multi-GPU only), 3 unused, 4 the fused tail (merge of the
+ * candidate lists + predictor + A5 + assignment), 5 unused (the assignment runs
+ * inside the tail), 6 insert (K0). */
 #define ARGUS_STAGE_PREP 0
 #define ARGUS_STAGE_SCAN 1
 #define ARGUS_STAGE_MERGE_LOCAL 2
 #define ARGUS_STAGE_MERGE_GLOBAL 3
-#define ARGUS_STAGE_MLP 4
+#define ARGUS_STAGE_TAIL 4
 #define ARGUS_STAGE_ASSIGN 5
 #define ARGUS_STAGE_INSERT 6
 #define ARGUS_NUM_STAGES 7

@@ -34,7 +34,7 @@ SYMBOLS = (
     "argus_get_stream", "argus_profile_enable", "argus_profile_read", "argus_route_destroy",
     "argus_strerror",
 )
-STAGES = ("prep", "scan", "merge_local", "merge_global", "mlp", "assign", "insert")
+STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
 
 class argus_option(C.Structure):

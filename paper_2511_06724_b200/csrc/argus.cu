@@ -30,9 +30,6 @@ namespace {
 
 constexpr int64_t INSERT_CHUNK = 1 << 16;  // rows per staged insert chunk
 
-struct QuotaArg {
-  int32_t c[32];
-};
 
 // NCCL is resolved lazily with dlopen (reusing an already-loaded libnccl.so.2,
 // e.g. torch's) so that loading libargus never pins a second NCCL into a process.
@@ -94,6 +91,8 @@ struct argus_router {
   float* d_W2 = nullptr;           // [L][H]
   float* d_h = nullptr;            // [n16][H] predictor hidden activations
   int32_t* d_mlp_cnt = nullptr;    // [n16 / 16] last-CTA tickets
+  int32_t* d_tail_cnt = nullptr;   // [1] last-block ticket
+  size_t tail_smem = 0;            // dynamic smem of the fused tail kernel
   float* d_b2 = nullptr;
   // cache shard (device)
   __nv_bfloat16* d_Cb = nullptr;
@@ -349,7 +348,7 @@ int argus_route_destroy(argus_router* r) {
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
   void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xF,  r->d_W1sT,     r->d_b1,
-                  r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
+                  r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt, r->d_tail_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
                   r->d_order, r->d_gthr};
@@ -375,7 +374,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
   if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
   if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
-  if (mlp_smem_bytes(c.d, c.k, c.hidden, c.L) > 227 * 1024) return ARGUS_E_INVALID;
+  if (tail_smem_bytes(c.d, c.k, c.hidden, c.L, c.max_batch) > 200 * 1024) return ARGUS_E_INVALID;
   if (c.max_batch < 1 || c.max_batch > 8192) return ARGUS_E_INVALID;
   if (c.capacity < 0 || c.capacity > 0xFFFFFFFELL) return ARGUS_E_INVALID;
   if (!(c.delta > 0.f && c.delta <= 1.f)) return ARGUS_E_INVALID;
@@ -439,6 +438,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   const int64_t n16 = ((int64_t)c.max_batch + 15) / 16 * 16;
   TRY_RC(dalloc(r, &r->d_h, (size_t)n16 * H));
   TRY_RC(dalloc(r, &r->d_mlp_cnt, (size_t)n16 / 16));
+  TRY_RC(dalloc(r, &r->d_tail_cnt, 1));
+  r->tail_smem = tail_smem_bytes(d, k, H, L, c.max_batch);
   TRY_RC(dalloc(r, &r->d_b2, L));
   TRY_RC(dalloc(r, &r->d_Cb, (size_t)(r->cap_local + 256) * d));
   TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
@@ -473,7 +474,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_flags, 0, sizeof(uint32_t), r->stream) != cudaSuccess ||
-      cudaMemsetAsync(r->d_mlp_cnt, 0, sizeof(int32_t) * (size_t)(n16 / 16), r->stream) != cudaSuccess) {
+      cudaMemsetAsync(r->d_mlp_cnt, 0, sizeof(int32_t) * (size_t)(n16 / 16), r->stream) != cudaSuccess ||
+      cudaMemsetAsync(r->d_tail_cnt, 0, sizeof(int32_t), r->stream) != cudaSuccess) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
@@ -618,18 +620,20 @@ static int64_t local_rows(const argus_router* r) {
   return (r->m_global + G - 1 - rk) / G;
 }
 
-static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, uint32_t* idx_dev,
-                        float* score_dev);
+// K6 + scan (+ K5 local merge into keys_dev when keys_dev != NULL).  *P_out receives
+// the number of per-range candidate lists left in d_partial.
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out);
 
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
-  return partial_impl(r, prompts_dev, N, keys_dev, nullptr, nullptr);
+  if (!keys_dev) return ARGUS_E_INVALID;
+  int32_t P = 0;
+  return partial_impl(r, prompts_dev, N, keys_dev, &P);
 }
 
-static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, uint32_t* idx_dev,
-                        float* score_dev) {
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out) {
   int rc = check_state(r);
   if (rc) return rc;
-  if (N < 1 || N > r->cfg.max_batch || !keys_dev) return ARGUS_E_INVALID;
+  if (N < 1 || N > r->cfg.max_batch) return ARGUS_E_INVALID;
   const bool root = r->cfg.rank == 0 || !nccl_mode(r);
   if (root && !prompts_dev) return ARGUS_E_INVALID;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
@@ -670,58 +674,54 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     else launch_scan(a, &r->tmap_c, &r->tmap_q, r->stream);
   }
   LAUNCHED(r);
-  {
-    StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
-    launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, idx_dev, score_dev, r->stream);
+  *P_out = a.P;
+  if (keys_dev) {
+    {
+      StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
+      launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
+    }
+    LAUNCHED(r);
   }
-  LAUNCHED(r);
   return ARGUS_OK;
 }
 
-static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N, const int32_t* quota,
+// The fused tail (merge of P candidate lists per prompt, predictor, A5, assignment).
+static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, bool merged);
+                       uint8_t* status_dev);
 
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
                            float* topk_score_dev, float* quality_dev, uint8_t* status_dev) {
+  if (G < 1 || !keys_all_dev) return ARGUS_E_INVALID;
   return finish_impl(r, keys_all_dev, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                     status_dev, false);
+                     status_dev);
 }
 
-// merged: the single-shard path already decoded ids / scores in its local merge.
-static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N, const int32_t* quota,
+static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, bool merged) {
+                       uint8_t* status_dev) {
   int rc = check_state(r);
   if (rc) return rc;
-  if (N < 1 || N > r->cfg.max_batch || G < 1 || !keys_all_dev || !quota) return ARGUS_E_INVALID;
+  if (N < 1 || N > r->cfg.max_batch || P < 1 || !keys_in || !quota) return ARGUS_E_INVALID;
   const int L = r->cfg.L, k = r->cfg.k;
-  QuotaArg q{};
-  for (int v = 0; v < L; ++v) {
+  for (int v = 0; v < L; ++v)
     if (quota[v] < 0) return ARGUS_E_INVALID;
-    q.c[v] = quota[v];
-  }
   CU_TRY(r, cudaSetDevice(r->cfg.device));
-  float* score = topk_score_dev ? topk_score_dev : r->d_score;
-  uint32_t* idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
-  if (!merged) {
-    {
-      StageScope sc(r, ARGUS_STAGE_MERGE_GLOBAL);
-      launch_merge_topk(keys_all_dev, G, N, k, r->d_keys, idx, score, r->stream);
-    }
-    LAUNCHED(r);
-  }
-  MlpArgs m{};
+  TailArgs m{};
+  m.keys_in = keys_in;
+  m.P = P;
+  m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
+  m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
   m.Xb = r->d_Xb;
-  m.topk_score = score;
   m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;
   m.W2 = r->d_W2;
+  m.b2 = r->d_b2;
   m.hbuf = r->d_h;
   m.block_cnt = r->d_mlp_cnt;
-  m.b2 = r->d_b2;
+  m.launch_cnt = r->d_tail_cnt;
   m.kskip = r->d_kskip;
   m.pth = r->d_pth;
   m.gate = r->d_gate;
@@ -731,33 +731,19 @@ static int finish_impl(argus_router* r, const uint64_t* keys_all_dev, int32_t G,
   m.k = k;
   m.H = r->cfg.hidden;
   m.L = L;
+  m.Lw = (L + 3) / 4 * 4;
   m.rhat = quality_dev ? quality_dev : r->d_rhat;
   m.rankof = r->d_pref;
-  m.Lw = (L + 3) / 4 * 4;
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
-  uint8_t* status = status_dev ? status_dev : r->d_status;
-  m.status = status;
-  {
-    StageScope sc(r, ARGUS_STAGE_MLP);
-    launch_mlp(m, r->stream);
-  }
-  LAUNCHED(r);
-  AssignArgs as{};
-  as.rankof = r->d_pref;
-  as.ccount = r->d_ccount;
-  as.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
-  for (int v = 0; v < 32; ++v) as.quota[v] = v < L ? q.c[v] : 0;
-  as.N = N;
-  as.L = L;
-  as.order = r->d_order;
-  as.option_out = option_out_dev ? option_out_dev : r->d_option;
-  as.status = status;
-  as.flags = r->d_flags;
+  for (int v = 0; v < 32; ++v) m.quota[v] = v < L ? quota[v] : 0;
+  m.option_out = option_out_dev ? option_out_dev : r->d_option;
+  m.status = status_dev ? status_dev : r->d_status;
+  m.flags = r->d_flags;
   {
-    StageScope sc(r, ARGUS_STAGE_ASSIGN);
-    launch_assign(as, r->stream);
+    StageScope sc(r, ARGUS_STAGE_TAIL);
+    launch_tail(m, r->tail_smem, r->stream);
   }
   LAUNCHED(r);
   return ARGUS_OK;
@@ -774,18 +760,19 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
   for (int v = 0; v < r->cfg.L; ++v)
     if (quota[v] < 0) return ARGUS_E_INVALID;
   r->pending = true;
-  if (!nccl_mode(r)) {  // single shard: the local merge is final and decodes ids / scores directly
-    rc = partial_impl(r, prompts_dev, N, r->d_keys, topk_idx_dev, topk_score_dev);
+  int32_t P = 0;
+  if (!nccl_mode(r)) {  // single shard: the tail merges the per-range lists directly
+    rc = partial_impl(r, prompts_dev, N, nullptr, &P);
     if (rc) return rc;
-    return finish_impl(r, r->d_keys, 1, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                       status_dev, true);
+    return finish_impl(r, r->d_partial, P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
+                       status_dev);
   }
-  rc = partial_impl(r, prompts_dev, N, r->d_keys, nullptr, nullptr);
+  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P);
   if (rc) return rc;
   // C-2: N*k candidate keys from every shard
   NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
   return finish_impl(r, r->d_keys_all, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
-                     quality_dev, status_dev, false);
+                     quality_dev, status_dev);
 }
 
 int argus_sync(argus_router* r) {

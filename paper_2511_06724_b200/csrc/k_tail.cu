@@ -1,0 +1,454 @@
+// k_tail.cu -- everything after the scan, in ONE launch:
+//
+//   phase M  (every CTA)     merge the P candidate lists of its 16 prompts into the
+//                            final top-k (K5 semantics; CTAs of a prompt block merge
+//                            redundantly, blockIdx.y == 0 writes topk_idx / topk_score)
+//   phase 1  (every CTA)     predictor layer 1 for 16 prompts x 32 hidden units:
+//                            h = relu(W1x . bf16(x) + W1s . s + b1)
+//   phase 2  (last CTA of a  layer 2 r_v = 1/(1+exp(-(W2 . h + b2)_v)), r_0 := 1 and A5:
+//            prompt block)     A_i = {v : v = 0 or k_skip_v = 0 or s_i1 >= tau_v}
+//                              C_i = {v in A_i : r_v >= delta}
+//                              pi_i = A_i by (r desc, p_th desc, v asc)
+//   phase 3  (last CTA of    priority (|C_i| asc, i asc) counting sort + serial dictatorship
+//            the launch)       under the quotas c_v
+//
+// The "last CTA" elections are atomic tickets (reset by the winner for the next
+// launch).  Fusing the four steps removes three kernel boundaries per batch; the
+// only redundant work is the 8-fold merge of each prompt block's candidates.
+//
+// Layer 1 runs on mma.sync m16n8k16 (bf16, fp32 accumulate): the whole predictor is
+// < 0.03 % of the scan's flops and this product (16 x d x 32 per CTA) is far below a
+// tcgen05 tile.  W1x is pre-arranged at init in per-lane fragment order so each B
+// fragment is one coalesced 8-byte load.  In phase 2 one warp owns one prompt and
+// lane v owns option v (L <= 32): masks are ballots, the preference rank is a
+// 32-lane compare-count, stored as the inverse permutation rank_i(v) that phase 3
+// consumes.  Phase 3 walks the prompts in priority order in one warp with lane v
+// holding rem_v and rank_i(v): one REDUX.MIN per prompt picks "the first option of
+// pi_i with quota left".
+#include "common.cuh"
+#include "kernels.h"
+
+namespace argus {
+
+constexpr int PB = 16;  // prompts per block (the MMA M dimension)
+constexpr int TT = 256;  // threads per CTA
+constexpr int TW = TT / 32;
+constexpr int NB = 33;   // |C_i| in [1, 32]
+constexpr int CH = 1024; // prompts per staged assignment chunk
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint2 b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+}
+
+__device__ __forceinline__ uint64_t half_max_u64(uint64_t x) {  // max over the 16 lanes of a half-warp
+#pragma unroll
+  for (int m = 8; m > 0; m >>= 1) {
+    const uint64_t y = shfl_xor_u64(x, m);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+
+static size_t phase1_bytes(int d, int k) {
+  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)TW * PB * 32 + (size_t)PB * k);
+}
+static size_t phase2_bytes(int H, int L) { return sizeof(float) * ((size_t)PB * H + (size_t)L * H); }
+static size_t phase3_bytes(int N, int L) {
+  const int Lw = (L + 3) / 4 * 4;
+  return sizeof(int32_t) * (size_t)N + (size_t)CH * Lw + sizeof(uint32_t) * CH + CH;
+}
+
+size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch) {
+  size_t b = phase1_bytes(d, k);
+  b = b > phase2_bytes(H, L) ? b : phase2_bytes(H, L);
+  b = b > phase3_bytes(max_batch, L) ? b : phase3_bytes(max_batch, L);
+  return b;
+}
+
+// ------------------------------------------------------------------ phase 3
+__device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
+  const int N = a.N, L = a.L, Lw = a.Lw;
+  int32_t* order_s = reinterpret_cast<int32_t*>(smraw);                  // [N]
+  uint8_t* rk_s = smraw + sizeof(int32_t) * (size_t)N;                   // [CH][Lw]
+  uint32_t* cm_s = reinterpret_cast<uint32_t*>(rk_s + (size_t)CH * Lw);  // [CH]
+  uint8_t* opt_s = reinterpret_cast<uint8_t*>(cm_s + CH);                 // [CH] (option | 0x80 overflow)
+  __shared__ int32_t base[NB];
+  __shared__ int32_t tot[NB];
+  __shared__ int32_t wcnt[TW][NB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // stable counting sort of prompts by |C_i|
+  if (tid < NB) base[tid] = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < N; i0 += TT) {  // warp-aggregated histogram
+    const int i = i0 + tid;
+    const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&base[b], __popc(peers));
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 33 bucket counts
+    const int c0 = base[lane];
+    int x = c0;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, m);
+      if (lane >= m) x += y;
+    }
+    const int tot31 = __shfl_sync(0xffffffffu, x, 31);
+    base[lane] = x - c0;
+    if (lane == 0) base[32] = tot31;
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < N; c0 += TT) {
+    const int i = c0 + tid;
+    const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
+    for (int x = tid; x < TW * NB; x += TT) (&wcnt[0][0])[x] = 0;
+    __syncthreads();
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    const int wrank = __popc(peers & ((1u << lane) - 1u));
+    if (b >= 0 && wrank == 0) wcnt[warp][b] = __popc(peers);
+    __syncthreads();
+    if (tid < NB) {
+      int run = 0;
+#pragma unroll
+      for (int w = 0; w < TW; ++w) { const int c = wcnt[w][tid]; wcnt[w][tid] = run; run += c; }
+      tot[tid] = run;
+    }
+    __syncthreads();
+    if (b >= 0) order_s[base[b] + wcnt[warp][b] + wrank] = i;
+    __syncthreads();
+    if (tid < NB) base[tid] += tot[tid];
+  }
+  __syncthreads();
+
+  // serial dictatorship over staged chunks
+  int rem = lane < L ? a.quota[lane] : 0;  // warp 0 only
+  bool any_overflow = false;
+  const int W = Lw / 4;
+  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.rankof);
+  for (int c0 = 0; c0 < N; c0 += CH) {
+    const int n = min(CH, N - c0);
+    for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
+      int ii[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * TT;
+        ii[u] = t < n ? order_s[c0 + t] : -1;
+      }
+      uint32_t cm[4];
+      uint32_t wd[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cm[u] = ii[u] >= 0 ? __ldcg(a.cmask + ii[u]) : 0u;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) wd[u][w] = (ii[u] >= 0 && w < W) ? __ldcg(rk32 + (int64_t)ii[u] * W + w) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * TT;
+        if (t < n) {
+          cm_s[t] = cm[u];
+#pragma unroll
+          for (int w = 0; w < 8; ++w)
+            if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = wd[u][w];
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t nxt = lane < L ? rk_s[lane] : 0xFFu;
+      for (int t = 0; t < n; ++t) {
+        const uint32_t rk = nxt;
+        if (t + 1 < n) nxt = lane < L ? rk_s[(size_t)(t + 1) * Lw + lane] : 0xFFu;
+        const uint32_t cand = (rk != 0xFFu && rem > 0) ? rk : 0xFFu;
+        const uint32_t best = __reduce_min_sync(0xffffffffu, cand);
+        const bool mine = best != 0xFFu && cand == best;  // positions are distinct: one lane
+        rem -= mine ? 1 : 0;
+        const uint32_t who = __ballot_sync(0xffffffffu, mine);  // off the loop-carried chain
+        if (lane == 0) opt_s[t] = who ? (uint8_t)(__ffs(who) - 1) : (uint8_t)0x80;
+        any_overflow |= (who == 0);
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < n; t += TT) {
+      const int i = order_s[c0 + t];
+      const int o = opt_s[t] & 0x7F;
+      uint8_t st = __ldcg(a.status + i);
+      if (opt_s[t] & 0x80) st |= 1u;         // ARGUS_ST_OVERFLOW (option 0)
+      if (!((cm_s[t] >> o) & 1u)) st |= 2u;  // ARGUS_ST_NONCOMPLIANT
+      a.status[i] = st;
+      a.option_out[i] = o;
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
+}
+
+// ------------------------------------------------------------------ the fused tail
+__global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __shared__ int is_last;
+  __shared__ uint64_t mk[PB][8];  // merged top-k keys of the block (k <= 8)
+  const int d = a.d, H = a.H, L = a.L, k = a.k;
+  const int RS = d + 8;                                               // padded bf16 row stride
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smraw);        // [PB][RS]
+  float* red = reinterpret_cast<float*>(smraw + (size_t)PB * RS * 2);  // [TW][PB*32]
+  float* ss = red + TW * PB * 32;                                     // [PB][k]
+  const int pb = blockIdx.x, cc = blockIdx.y;
+  const int i0 = pb * PB;
+  const int nP = min(PB, a.N - i0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();
+
+  // stage the prompt block (rows past N in Xb are zero padding) with async copies
+  for (int idx = tid; idx < PB * (d / 8); idx += TT) {
+    const int p = idx / (d / 8), c = idx - p * (d / 8);
+    cp_async16(xs + p * RS + c * 8, reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d) + c);
+  }
+  // per-thread epilogue constants of layer 1
+  float w1s_r[2][8], b1_r[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int j = cc * 32 + ((tid + u * TT) & 31);
+    b1_r[u] = __ldg(a.b1 + j);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
+  }
+
+  // ---- phase M: merge P lists of k keys for prompt (2 warp + half), one half-warp per prompt
+  {
+    const int hl = lane & 15, pl = 2 * warp + (lane >> 4);
+    const int i = i0 + pl;
+    TopList<8> tl;
+    tl.clear();
+    if (pl < nP) {
+      const int total = a.P * k;
+      constexpr int B = 8;
+      for (int e = hl; e < total; e += 16 * B) {
+        uint64_t buf[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int ee = e + u * 16;
+          uint64_t key = 0;
+          if (ee < total) {
+            const int p = ee / k, t = ee - p * k;
+            key = __ldcg(reinterpret_cast<const unsigned long long*>(a.keys_in) + ((int64_t)p * a.N + i) * k + t);
+          }
+          buf[u] = key;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) tl.insert(buf[u]);
+      }
+    }
+    for (int t = 0; t < k; ++t) {  // half-warp extraction (keys unique apart from 0)
+      const uint64_t m = half_max_u64(tl.v[0]);
+      if (hl == 0) mk[pl][t] = m;
+      if (m != 0 && tl.v[0] == m) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) tl.v[q] = tl.v[q + 1];
+        tl.v[7] = 0;
+      }
+    }
+    __syncwarp();
+    if (pl < nP && hl < k) {
+      const uint64_t key = mk[pl][hl];
+      ss[pl * k + hl] = key_score(key);
+      if (cc == 0) {
+        a.topk_idx[(int64_t)i * k + hl] = key_id(key);
+        a.topk_score[(int64_t)i * k + hl] = key_score(key);
+      }
+    } else if (pl >= nP && hl < k) {
+      ss[pl * k + hl] = 0.f;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- phase 1: hidden units [32 cc, 32 cc + 32), warp w takes a 1/8 slice of d
+  {
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
+    const int RSW = RS / 2;
+    const int KS = d / 16;
+    const int ks0 = KS * warp / TW, ks1 = KS * (warp + 1) / TW;
+    const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
+    float acc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+    constexpr int KSW = 8;  // k-steps per warp for d <= 1024: all B fragments in one round trip
+    uint2 bf[KSW][4];
+#pragma unroll
+    for (int q = 0; q < KSW; ++q)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        bf[q][nt] = (ks0 + q < ks1) ? __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks0 + q) * 32 + lane) : make_uint2(0, 0);
+#pragma unroll
+    for (int q = 0; q < KSW; ++q) {
+      if (ks0 + q < ks1) {
+        const int ks = ks0 + q;
+        uint32_t af[4];
+        af[0] = x32[g * RSW + ks * 8 + t];
+        af[1] = x32[(g + 8) * RSW + ks * 8 + t];
+        af[2] = x32[g * RSW + ks * 8 + 4 + t];
+        af[3] = x32[(g + 8) * RSW + ks * 8 + 4 + t];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_bf16_16816(acc[nt], af, bf[q][nt]);
+      }
+    }
+    float* rw = red + warp * PB * 32;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rw[(g + (e >> 1) * 8) * 32 + nt * 8 + 2 * t + (e & 1)] = acc[nt][e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {  // PB * 32 = 2 * TT: reduce split-K partials in a fixed order
+    const int e = tid + u * TT;
+    const int row = e >> 5, j = cc * 32 + (e & 31);
+    float z = 0.f;
+#pragma unroll
+    for (int w = 0; w < TW; ++w) z = __fadd_rn(z, red[w * PB * 32 + e]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < k) z = __fmaf_rn(w1s_r[u][q], ss[row * k + q], z);
+    a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, b1_r[u]), 0.f);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) is_last = atomicAdd(&a.block_cnt[pb], 1) == (int)gridDim.y - 1;
+  __syncthreads();
+  pdl_launch();
+  if (!is_last) return;
+
+  // ---- phase 2: layer 2 + A5 for the 16 prompts of this block
+  __threadfence();
+  if (tid == 0) a.block_cnt[pb] = 0;  // ready for the next launch
+  float s1_r[PB / TW];
+#pragma unroll
+  for (int r = 0; r < PB / TW; ++r) {
+    const int p = warp + r * TW;
+    s1_r[r] = p < nP ? ss[p * k] : 0.f;
+  }
+  __syncthreads();  // ss (inside the staging area) is overwritten below
+  float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]
+  float* w2s = hs + PB * H;                     // [L][H]
+  for (int e = tid; e < PB * H / 4; e += TT) cp_async16(hs + 4 * e, a.hbuf + (int64_t)i0 * H + 4 * e);
+  for (int e = tid; e < L * H / 4; e += TT) cp_async16(w2s + 4 * e, a.W2 + 4 * e);
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PB / TW; ++r) {
+    const int p = warp + r * TW;
+    if (p >= nP) break;
+    const int i = i0 + p;
+    const bool act = lane < L;
+    float part[32];
+#pragma unroll
+    for (int v = 0; v < 32; ++v) part[v] = 0.f;
+    for (int j = lane; j < H; j += 32) {
+      const float hj = hs[p * H + j];
+#pragma unroll
+      for (int v = 0; v < 32; ++v)
+        if (v < L) part[v] = __fmaf_rn(w2s[v * H + j], hj, part[v]);
+    }
+    float z = 0.f;
+#pragma unroll
+    for (int v = 0; v < 32; ++v) {
+      if (v < L) {
+        float sv = part[v];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, m));
+        if (lane == v) z = sv;
+      }
+    }
+    float rr = 0.f;
+    if (act) {
+      z = __fadd_rn(z, a.b2[lane]);
+      rr = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
+      if (lane == 0) rr = 1.0f;
+    }
+    const float s1 = s1_r[r];
+    const int ks_ = act ? a.kskip[lane] : 0;
+    const float gate = act ? a.gate[lane] : 0.f;
+    const bool gated_pass = act && ks_ != 0 && s1 >= gate;
+    const bool adm = act && (lane == 0 || ks_ == 0 || s1 >= gate);
+    const bool cmp = adm && rr >= a.delta;
+    const uint32_t amask = __ballot_sync(0xffffffffu, adm);
+    const uint32_t cmask = __ballot_sync(0xffffffffu, cmp);
+    const uint32_t gmask = __ballot_sync(0xffffffffu, act && ks_ != 0);
+    const uint32_t pmask = __ballot_sync(0xffffffffu, gated_pass);
+    const float pth = act ? a.pth[lane] : 0.f;
+    int rank = 0;
+    for (int u = 0; u < L; ++u) {
+      const float ru = __shfl_sync(0xffffffffu, rr, u);
+      const float pu = __shfl_sync(0xffffffffu, pth, u);
+      const bool before = ((amask >> u) & 1u) &&
+                          (ru > rr || (ru == rr && (pu > pth || (pu == pth && u < lane))));
+      rank += before ? 1 : 0;
+    }
+    if (act) {
+      a.rhat[(int64_t)i * L + lane] = rr;
+      a.rankof[(int64_t)i * a.Lw + lane] = adm ? (uint8_t)rank : (uint8_t)0xFF;  // position of v in pi_i
+    } else if (lane < a.Lw) {
+      a.rankof[(int64_t)i * a.Lw + lane] = 0xFF;
+    }
+    if (lane == 0) {
+      a.ccount[i] = (uint8_t)__popc(cmask);
+      a.cmask[i] = cmask;
+      a.status[i] = (gmask != 0 && pmask == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
+    }
+  }
+
+  // ---- phase 3: the last block to finish phase 2 runs the assignment for all N
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) is_last = atomicAdd(a.launch_cnt, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (tid == 0) *a.launch_cnt = 0;
+  assign_all(a, smraw);
+}
+
+// W1x [H][d] (fp32 rows of w1 [H][d+k]) -> bf16 (RNE) in mma.sync B-fragment order:
+// Wf[(nb * KS + ks) * 32 + lane] = {W[n][k0..k0+1], W[n][k0+8..k0+9]},
+// n = nb * 8 + lane / 4, k0 = ks * 16 + (lane % 4) * 2.
+__global__ void k_prep_w1_frag(const float* __restrict__ w1, int d, int k, int H, uint2* __restrict__ Wf) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int KS = d / 16;
+  const int64_t total = (int64_t)(H / 8) * KS * 32;
+  if (idx >= total) return;
+  const int lane = (int)(idx & 31);
+  const int64_t q = idx >> 5;
+  const int ks = (int)(q % KS), nb = (int)(q / KS);
+  const int n = nb * 8 + lane / 4, k0 = ks * 16 + (lane % 4) * 2;
+  const float* row = w1 + (int64_t)n * (d + k);
+  __nv_bfloat162 lo = __floats2bfloat162_rn(row[k0], row[k0 + 1]);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(row[k0 + 8], row[k0 + 9]);
+  Wf[idx] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s) {
+  const int64_t total = (int64_t)(H / 8) * (d / 16) * 32;
+  k_prep_w1_frag<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(w1, d, k, H, reinterpret_cast<uint2*>(Wf));
+}
+
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s) {
+  static size_t attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = smem;
+  }
+  const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
+  launch_pdl(k_tail, grid, dim3(TT), smem, s, a);
+}
+
+}  // namespace argus

@@ -65,46 +65,42 @@ void launch_scan_simt(const ScanArgs& a, cudaStream_t s);
 void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint64_t* keys_out,
                        uint32_t* idx_out, float* score_out, cudaStream_t s);
 
-struct MlpArgs {
+struct TailArgs {
+  // phase M: candidate lists -> final top-k
+  const uint64_t* keys_in;   // [P][N][k] candidate keys (per-range partials, or all-gathered shards)
+  int32_t P;
+  uint32_t* topk_idx;        // [N][k] out
+  float* topk_score;         // [N][k] out
+  // predictor
   const __nv_bfloat16* Xb;   // [n_pad][d]
-  const float* topk_score;   // [N][k]
   const void* W1xF;          // W1x bf16 in mma.sync B-fragment order (see k_prep_w1_frag)
   const float* W1sT;         // [k][H]
   const float* b1;           // [H]
   const float* W2;           // [L][H]
-  float* hbuf;               // [ceil(N/16)*16][H] hidden activations (scratch)
-  int32_t* block_cnt;        // [ceil(max_batch/16)] zeroed tickets (last-CTA election)
   const float* b2;           // [L]
+  float* hbuf;               // [ceil(N/16)*16][H] hidden activations (scratch)
+  int32_t* block_cnt;        // [ceil(max_batch/16)] zeroed tickets (last CTA of a prompt block)
+  int32_t* launch_cnt;       // [1] zeroed ticket (last block of the launch)
+  // A5
   const int32_t* kskip;      // [L]
   const float* pth;          // [L]
   const float* gate;         // [L]
   float delta;
-  int32_t N, d, k, H, L;
-  float* rhat;               // [N][L]
+  int32_t N, d, k, H, L, Lw; // Lw = L rounded up to 4 (rankof row stride)
+  float* rhat;               // [N][L] out
   uint8_t* rankof;           // [N][Lw] position of option v in pi_i (0xFF: not admissible)
-  int32_t Lw;                // row stride of rankof: L rounded up to 4
   uint8_t* ccount;           // [N] |C_i|
   uint32_t* cmask;           // [N] compliance mask
-  uint8_t* status;           // [N] base status bits (GATED_ALL)
-};
-// K3 + A5: predictor MLP with fused compliance / preference / priority keys.
-void launch_mlp(const MlpArgs& a, cudaStream_t s);
-size_t mlp_smem_bytes(int d, int k, int H, int L);
-// init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
-void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
-
-struct AssignArgs {
-  const uint8_t* rankof;     // [N][Lw] position of option v in pi_i (0xFF: not admissible)
-  const uint8_t* ccount;
-  const uint32_t* cmask;
-  int32_t quota[32];         // [L] per-option quotas c_v (by value)
-  int32_t N, L;
-  int32_t* order;            // [N] scratch: priority order
-  int32_t* option_out;       // [N]
-  uint8_t* status;           // [N] in: base bits, out: + OVERFLOW / NONCOMPLIANT
+  // A6
+  int32_t quota[32];         // per-option quotas c_v (by value)
+  int32_t* option_out;       // [N] out
+  uint8_t* status;           // [N] out
   uint32_t* flags;
 };
-// K4: priority counting sort + serial dictatorship.
-void launch_assign(const AssignArgs& a, cudaStream_t s);
+// K3+K4 (+K5 on one GPU): merge, predictor, A5 and the assignment in one launch.
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s);
+size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch);
+// init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
+void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
 
 }  // namespace argus

@@ -226,7 +226,11 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     const int i = i0 + pl;
     TopList<8> tl;
     tl.clear();
-    if (pl < nP) {
+    const int cnt = (a.cand && pl < nP) ? __ldcg(a.cand_cnt + i) : CAND_CAP + 1;
+    if (pl < nP && cnt <= CAND_CAP) {  // compact path: the few candidates at or above the shared bound
+      for (int e = hl; e < cnt; e += 16)
+        tl.insert(__ldcg(reinterpret_cast<const unsigned long long*>(a.cand) + (int64_t)i * CAND_CAP + e));
+    } else if (pl < nP) {            // full path: every list (multi-GPU, or compact overflow)
       const int total = a.P * k;
       constexpr int B = 8;
       for (int e = hl; e < total; e += 16 * B) {

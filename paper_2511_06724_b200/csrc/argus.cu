@@ -102,8 +102,6 @@ struct argus_router {
   __nv_bfloat16* d_Xb = nullptr;   // [n_pad_max][d]
   float* d_invq = nullptr;         // [n_pad_max]
   uint64_t* d_gthr = nullptr;      // [n_pad_max] shared per-prompt scan threshold
-  uint64_t* d_cand = nullptr;      // [n_pad_max][CAND_CAP] compact candidates
-  int32_t* d_cand_cnt = nullptr;   // [n_pad_max]
   uint64_t* d_partial = nullptr;   // [p_max][max_batch][k]
   uint64_t* d_keys = nullptr;      // [max_batch][k]
   uint64_t* d_keys_all = nullptr;  // [world][max_batch][k]
@@ -353,7 +351,7 @@ int argus_route_destroy(argus_router* r) {
                   r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt, r->d_tail_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
                   r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
                   r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
-                  r->d_order, r->d_gthr, r->d_cand, r->d_cand_cnt};
+                  r->d_order, r->d_gthr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -376,7 +374,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
   if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
   if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
-  if (tail_smem_bytes(c.d, c.k, c.hidden, c.L, c.max_batch) > 200 * 1024) return ARGUS_E_INVALID;
+  if (tail_smem_bytes(c.d, c.k, c.hidden, c.L, c.max_batch, 148) > 220 * 1024) return ARGUS_E_INVALID;
   if (c.max_batch < 1 || c.max_batch > 8192) return ARGUS_E_INVALID;
   if (c.capacity < 0 || c.capacity > 0xFFFFFFFELL) return ARGUS_E_INVALID;
   if (!(c.delta > 0.f && c.delta <= 1.f)) return ARGUS_E_INVALID;
@@ -441,7 +439,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_h, (size_t)n16 * H));
   TRY_RC(dalloc(r, &r->d_mlp_cnt, (size_t)n16 / 16));
   TRY_RC(dalloc(r, &r->d_tail_cnt, 1));
-  r->tail_smem = tail_smem_bytes(d, k, H, L, c.max_batch);
+  r->tail_smem = tail_smem_bytes(d, k, H, L, c.max_batch, std::max(r->num_sms, c.world));
   TRY_RC(dalloc(r, &r->d_b2, L));
   TRY_RC(dalloc(r, &r->d_Cb, (size_t)(r->cap_local + 256) * d));
   TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
@@ -449,8 +447,6 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_Xb, (size_t)r->n_pad_max * d));
   TRY_RC(dalloc(r, &r->d_invq, (size_t)r->n_pad_max));
   TRY_RC(dalloc(r, &r->d_gthr, (size_t)r->n_pad_max));
-  TRY_RC(dalloc(r, &r->d_cand, (size_t)r->n_pad_max * CAND_CAP));
-  TRY_RC(dalloc(r, &r->d_cand_cnt, (size_t)r->n_pad_max));
   TRY_RC(dalloc(r, &r->d_partial, (size_t)r->p_max * c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
@@ -646,14 +642,10 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
     StageScope sc(r, ARGUS_STAGE_PREP);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_gthr, r->d_cand_cnt, r->d_flags,
-                        r->stream);
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_gthr, r->d_flags, r->stream);
     LAUNCHED(r);
   }
-  if (!root) {
-    CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
-    CU_TRY(r, cudaMemsetAsync(r->d_cand_cnt, 0, sizeof(int32_t) * (size_t)n_pad, r->stream));
-  }
+  if (!root) CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
   if (nccl_mode(r)) {
     NC_TRY(r, nccl().GroupStart());
     NC_TRY(r, nccl().Broadcast(r->d_Xb, r->d_Xb, (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
@@ -674,8 +666,6 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.world = r->cfg.world;
   a.partial = r->d_partial;
   a.gthr = r->d_gthr;
-  a.cand = r->d_cand;
-  a.cand_cnt = r->d_cand_cnt;
   a.P = std::min(r->scan_simt ? scan_plan_ranges_simt(a.m_local, N, r->num_sms)
                               : scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
   {
@@ -698,7 +688,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 // The fused tail (merge of P candidate lists per prompt, predictor, A5, assignment).
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, bool compact = false);
+                       uint8_t* status_dev);
 
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
@@ -710,7 +700,7 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
 
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, bool compact) {
+                       uint8_t* status_dev) {
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch || P < 1 || !keys_in || !quota) return ARGUS_E_INVALID;
@@ -721,8 +711,6 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   TailArgs m{};
   m.keys_in = keys_in;
   m.P = P;
-  m.cand = compact ? r->d_cand : nullptr;
-  m.cand_cnt = r->d_cand_cnt;
   m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
   m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
   m.Xb = r->d_Xb;
@@ -777,7 +765,7 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     rc = partial_impl(r, prompts_dev, N, nullptr, &P);
     if (rc) return rc;
     return finish_impl(r, r->d_partial, P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                       status_dev, !r->scan_simt);
+                       status_dev);
   }
   rc = partial_impl(r, prompts_dev, N, r->d_keys, &P);
   if (rc) return rc;

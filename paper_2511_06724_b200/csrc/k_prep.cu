@@ -52,15 +52,12 @@ __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t
 
 __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, int d,
                                __nv_bfloat16* __restrict__ Xb, float* __restrict__ inv_q,
-                               uint64_t* __restrict__ gthr, int32_t* __restrict__ cand_cnt, uint32_t* flags) {
+                               uint64_t* __restrict__ gthr, uint32_t* flags) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   pdl_wait();  // the previous batch's kernels may still read Xb / inv_q
   if (warp >= n_pad) return;
-  if (lane == 0) {  // the scan's shared per-prompt threshold and candidate list start empty
-    gthr[warp] = 0;
-    cand_cnt[warp] = 0;
-  }
+  if (lane == 0) gthr[warp] = 0;  // the scan's shared per-prompt threshold starts empty
   if (warp >= N) {  // zero padding rows: score 0, never reported
     uint32_t* z = reinterpret_cast<uint32_t*>(Xb + (int64_t)warp * d);
     for (int j = lane; j < d / 2; j += 32) z[j] = 0u;
@@ -89,11 +86,10 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 }
 
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
-                         float* inv_q, uint64_t* gthr, int32_t* cand_cnt, uint32_t* flags, cudaStream_t s) {
+                         float* inv_q, uint64_t* gthr, uint32_t* flags, cudaStream_t s) {
   const int threads = 256;
   int blocks = (n_pad * 32 + threads - 1) / threads;
-  launch_pdl(k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, cand_cnt,
-             flags);
+  launch_pdl(k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, flags);
 }
 
 }  // namespace argus

@@ -324,19 +324,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2)
         if (t2 < a.k) out[t2] = tl.v[t2];
-      // compact candidates: only entries >= the shared bound can be in the prompt's top-k
-      // (the bound only rises, so reading it now is conservative); typically a handful
-      // per prompt instead of P * k.  Overflow past CAND_CAP leaves the full lists as truth.
-      const uint64_t gnow = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
-      int n = 0;
-#pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2) n += (t2 < a.k && tl.v[t2] != 0 && tl.v[t2] >= gnow) ? 1 : 0;
-      if (n > 0) {
-        const int base = atomicAdd(a.cand_cnt + p, n);
-#pragma unroll
-        for (int t2 = 0; t2 < KMAX; ++t2)
-          if (t2 < n && base + t2 < CAND_CAP) a.cand[(int64_t)p * CAND_CAP + base + t2] = tl.v[t2];
-      }
     }
   }
 

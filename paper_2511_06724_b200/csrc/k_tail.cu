@@ -25,10 +25,22 @@
 // consumes.  Phase 3 walks the prompts in priority order in one warp with lane v
 // holding rem_v and rank_i(v): one REDUX.MIN per prompt picks "the first option of
 // pi_i with quota left".
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef ARGUS_TAIL_TIMING
+#define ARGUS_TAIL_TIMING 0  // diagnostics build only: device printf of phase timestamps
+#endif
+
 namespace argus {
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int PB = 16;  // prompts per block (the MMA M dimension)
 constexpr int TT = 256;  // threads per CTA
@@ -53,17 +65,18 @@ __device__ __forceinline__ uint64_t half_max_u64(uint64_t x) {  // max over the 
   return x;
 }
 
-static size_t phase1_bytes(int d, int k) {
-  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)TW * PB * 32 + (size_t)PB * k);
+static size_t phase1_bytes(int d, int k, int P_max) {
+  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)TW * PB * 32 + (size_t)PB * 8) +
+         sizeof(uint64_t) * (size_t)P_max * PB * k;
 }
-static size_t phase2_bytes(int H, int L) { return sizeof(float) * ((size_t)PB * H + (size_t)L * H); }
+static size_t phase2_bytes(int H, int L) { return sizeof(float) * ((size_t)PB * H + (size_t)L * (H + 4)); }
 static size_t phase3_bytes(int N, int L) {
   const int Lw = (L + 3) / 4 * 4;
   return sizeof(int32_t) * (size_t)N + (size_t)CH * Lw + sizeof(uint32_t) * CH + CH;
 }
 
-size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch) {
-  size_t b = phase1_bytes(d, k);
+size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max) {
+  size_t b = phase1_bytes(d, k, P_max);
   b = b > phase2_bytes(H, L) ? b : phase2_bytes(H, L);
   b = b > phase3_bytes(max_batch, L) ? b : phase3_bytes(max_batch, L);
   return b;
@@ -203,7 +216,11 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   const int i0 = pb * PB;
   const int nP = min(PB, a.N - i0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t T[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t U[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ARGUS_TAIL_TIMING) T[0] = gtimer();
   pdl_wait();
+  if (ARGUS_TAIL_TIMING) T[1] = gtimer();
 
   // stage the prompt block (rows past N in Xb are zero padding) with async copies
   for (int idx = tid; idx < PB * (d / 8); idx += TT) {
@@ -220,35 +237,37 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
   }
 
-  // ---- phase M: merge P lists of k keys for prompt (2 warp + half), one half-warp per prompt
+  if (ARGUS_TAIL_TIMING) U[0] = gtimer();
+  // ---- phase M: merge the P lists of k keys of each prompt of the block.  All of the
+  // block's keys (P slabs of 16 prompts x k, contiguous per list) arrive with one burst of
+  // async copies; then one half-warp per prompt folds them from shared memory.
+  uint64_t* kst = reinterpret_cast<uint64_t*>(ss + PB * 8);  // [P][PB][k]
+  {
+    const int slab = PB * k / 2;  // 16-byte chunks per list
+    for (int x = tid; x < a.P * slab; x += TT) {
+      const int p = x / slab, c = x - p * slab;
+      if (i0 * k + 2 * c < a.N * k)  // prompts past N: left unfilled, never read
+        cp_async16(kst + (size_t)p * PB * k + 2 * c,
+                   reinterpret_cast<const uint4*>(a.keys_in + ((int64_t)p * a.N + i0) * k) + c);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (ARGUS_TAIL_TIMING) U[0] = gtimer();
   {
     const int hl = lane & 15, pl = 2 * warp + (lane >> 4);
     const int i = i0 + pl;
     TopList<8> tl;
     tl.clear();
-    const int cnt = (a.cand && pl < nP) ? __ldcg(a.cand_cnt + i) : CAND_CAP + 1;
-    if (pl < nP && cnt <= CAND_CAP) {  // compact path: the few candidates at or above the shared bound
-      for (int e = hl; e < cnt; e += 16)
-        tl.insert(__ldcg(reinterpret_cast<const unsigned long long*>(a.cand) + (int64_t)i * CAND_CAP + e));
-    } else if (pl < nP) {            // full path: every list (multi-GPU, or compact overflow)
+    if (pl < nP) {
       const int total = a.P * k;
-      constexpr int B = 8;
-      for (int e = hl; e < total; e += 16 * B) {
-        uint64_t buf[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-          const int ee = e + u * 16;
-          uint64_t key = 0;
-          if (ee < total) {
-            const int p = ee / k, t = ee - p * k;
-            key = __ldcg(reinterpret_cast<const unsigned long long*>(a.keys_in) + ((int64_t)p * a.N + i) * k + t);
-          }
-          buf[u] = key;
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u) tl.insert(buf[u]);
+#pragma unroll 1
+      for (int e = hl; e < total; e += 16) {
+        const int p = e / k, t = e - p * k;
+        tl.insert(kst[((size_t)p * PB + pl) * k + t]);
       }
     }
+    if (ARGUS_TAIL_TIMING) U[1] = gtimer();
     for (int t = 0; t < k; ++t) {  // half-warp extraction (keys unique apart from 0)
       const uint64_t m = half_max_u64(tl.v[0]);
       if (hl == 0) mk[pl][t] = m;
@@ -270,8 +289,9 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       ss[pl * k + hl] = 0.f;
     }
   }
-  cp_async_wait_all();
+  if (ARGUS_TAIL_TIMING) U[2] = gtimer();
   __syncthreads();
+  if (ARGUS_TAIL_TIMING) T[2] = gtimer();
 
   // ---- phase 1: hidden units [32 cc, 32 cc + 32), warp w takes a 1/8 slice of d
   {
@@ -325,6 +345,7 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       if (q < k) z = __fmaf_rn(w1s_r[u][q], ss[row * k + q], z);
     a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, b1_r[u]), 0.f);
   }
+  if (ARGUS_TAIL_TIMING) T[3] = gtimer();
   __threadfence();
   __syncthreads();
   if (tid == 0) is_last = atomicAdd(&a.block_cnt[pb], 1) == (int)gridDim.y - 1;
@@ -345,33 +366,38 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]
   float* w2s = hs + PB * H;                     // [L][H]
   for (int e = tid; e < PB * H / 4; e += TT) cp_async16(hs + 4 * e, a.hbuf + (int64_t)i0 * H + 4 * e);
-  for (int e = tid; e < L * H / 4; e += TT) cp_async16(w2s + 4 * e, a.W2 + 4 * e);
+  const int H4 = H + 4;  // padded W2 rows: lane v's float4 reads fall in different banks
+  for (int e = tid; e < L * H / 4; e += TT) {
+    const int v = e / (H / 4), j4 = e - v * (H / 4);
+    cp_async16(w2s + v * H4 + 4 * j4, a.W2 + 4 * e);
+  }
   cp_async_wait_all();
   __syncthreads();
+  if (ARGUS_TAIL_TIMING) U[3] = gtimer();
 #pragma unroll
   for (int r = 0; r < PB / TW; ++r) {
     const int p = warp + r * TW;
     if (p >= nP) break;
     const int i = i0 + p;
     const bool act = lane < L;
-    float part[32];
-#pragma unroll
-    for (int v = 0; v < 32; ++v) part[v] = 0.f;
-    for (int j = lane; j < H; j += 32) {
-      const float hj = hs[p * H + j];
-#pragma unroll
-      for (int v = 0; v < 32; ++v)
-        if (v < L) part[v] = __fmaf_rn(w2s[v * H + j], hj, part[v]);
-    }
+    // lane v owns option v: z_v = b2_v + sum_j W2[v][j] h_j, four interleaved partial
+    // sums in a compact (not unrolled) loop -- this phase runs once per CTA from a cold
+    // instruction cache, so code size, not arithmetic, is what costs here
     float z = 0.f;
-#pragma unroll
-    for (int v = 0; v < 32; ++v) {
-      if (v < L) {
-        float sv = part[v];
-#pragma unroll
-        for (int m = 16; m > 0; m >>= 1) sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, m));
-        if (lane == v) z = sv;
+    if (act) {
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      const float* w2r = w2s + lane * H4;
+      const float* hp = hs + p * H;
+#pragma unroll 1
+      for (int j = 0; j < H; j += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(w2r + j);
+        const float4 h4 = *reinterpret_cast<const float4*>(hp + j);
+        z0 = __fmaf_rn(w4.x, h4.x, z0);
+        z1 = __fmaf_rn(w4.y, h4.y, z1);
+        z2 = __fmaf_rn(w4.z, h4.z, z2);
+        z3 = __fmaf_rn(w4.w, h4.w, z3);
       }
+      z = __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));
     }
     float rr = 0.f;
     if (act) {
@@ -412,6 +438,7 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   }
 
   // ---- phase 3: the last block to finish phase 2 runs the assignment for all N
+  if (ARGUS_TAIL_TIMING) T[4] = gtimer();
   __threadfence();
   __syncthreads();
   if (tid == 0) is_last = atomicAdd(a.launch_cnt, 1) == (int)gridDim.x - 1;
@@ -419,7 +446,17 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   if (!is_last) return;
   __threadfence();
   if (tid == 0) *a.launch_cnt = 0;
+  if (ARGUS_TAIL_TIMING) T[5] = gtimer();
   assign_all(a, smraw);
+  if (ARGUS_TAIL_TIMING) {
+    T[6] = gtimer();
+    if (tid == 0)
+      printf("[tail] N=%d pdl %llu | pre-merge %llu loads %llu extract %llu cpwait %llu | layer1 %llu | ticket+stage2 %llu l2+A5 %llu | ticket %llu | assign %llu ns\n",
+             a.N, (unsigned long long)(T[1] - T[0]), (unsigned long long)(U[0] - T[1]),
+             (unsigned long long)(U[1] - U[0]), (unsigned long long)(U[2] - U[1]), (unsigned long long)(T[2] - U[2]),
+             (unsigned long long)(T[3] - T[2]), (unsigned long long)(U[3] - T[3]), (unsigned long long)(T[4] - U[3]),
+             (unsigned long long)(T[5] - T[4]), (unsigned long long)(T[6] - T[5]));
+  }
 }
 
 // W1x [H][d] (fp32 rows of w1 [H][d+k]) -> bf16 (RNE) in mma.sync B-fragment order:

@@ -39,10 +39,7 @@ struct ScanArgs {
   uint64_t* partial;         // [P][N][k] per-CTA-range candidates
   int32_t P;                 // number of cache ranges (filled by the planner)
   uint64_t* gthr;            // [n_pad] per-prompt shared top-k threshold key (zeroed by K6)
-  uint64_t* cand;            // [n_pad][CAND_CAP] compact candidates: list entries >= gthr at write time
-  int32_t* cand_cnt;         // [n_pad] entries appended to cand (zeroed by K6; > CAND_CAP = overflowed)
 };
-constexpr int CAND_CAP = 32;
 
 // K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
 // g % world == rank go to slot g / world.
@@ -52,7 +49,7 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 
 // K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
-                         float* inv_q, uint64_t* gthr, int32_t* cand_cnt, uint32_t* flags, cudaStream_t s);
+                         float* inv_q, uint64_t* gthr, uint32_t* flags, cudaStream_t s);
 
 // K1+K2: fused tcgen05 scan + per-range top-k -> partial [P][N][k].
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
@@ -72,8 +69,6 @@ struct TailArgs {
   // phase M: candidate lists -> final top-k
   const uint64_t* keys_in;   // [P][N][k] candidate keys (per-range partials, or all-gathered shards)
   int32_t P;
-  const uint64_t* cand;      // [n_pad][CAND_CAP] compact candidates, or NULL (then keys_in only)
-  const int32_t* cand_cnt;   // [n_pad]
   uint32_t* topk_idx;        // [N][k] out
   float* topk_score;         // [N][k] out
   // predictor
@@ -104,7 +99,7 @@ struct TailArgs {
 };
 // K3+K4 (+K5 on one GPU): merge, predictor, A5 and the assignment in one launch.
 void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s);
-size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch);
+size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max);
 // init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
 void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);
 

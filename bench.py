@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of fixed N: per-N stage times to stderr")
     ap.add_argument("--fixed-n", type=int, default=0, help="diagnostics: every batch has this N")
+    ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
+                    help="1: the tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline)")
     return ap.parse_args()
 
 
@@ -182,7 +184,8 @@ def main():
     uid = adist.share_nccl_id(dist, rank, argus.argus_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.Stream()
     r = argus.Router(d, k, opts, W1, b1, W2, b2, capacity=cfg.M, max_batch=max_batch, rank=rank, world=world,
-                     device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream)
+                     device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream,
+                     pipeline=bool(args.pipeline) and world == 1)
 
     # ---- cache: generated chunk by chunk, inserted through the ABI (rank 0 authoritative)
     cg = gen.CacheGen(cfg.M, d, cfg.seed)
@@ -231,6 +234,7 @@ def main():
             ev0.record(stream)
             for t in range(args.warmup, args.warmup + args.steps):
                 prompts += step(t)
+            r.argus_route_join()  # the router's stream waits for the last pipelined tail
             ev1.record(stream)
         ev1.synchronize()
     rc = r.argus_sync()
@@ -343,6 +347,9 @@ def main():
             "parallelism": f"cache row-striped over {world} GPU(s)",
             "l2": f"inputs larger than L2 (cache shard {bytes_per_launch / 1e9:.2f} GB >> 126 MB L2)",
             "insert_s": round(t_insert, 2),
+            "pipeline": ("tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline=1); every "
+                         "batch's outputs are complete inside the timed region")
+                        if (args.pipeline and world == 1) else "off",
         },
         "e2e": {"value": round(e2e_prompts / (e2e_ms / 1e3), 1), "unit": "prompts/s",
                 "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),

@@ -98,7 +98,14 @@ typedef struct {
  *   rank, world, device   this process's rank, world size (1 = single GPU), CUDA device
  *   nccl_unique_id        128-byte ncclUniqueId identical on all ranks, or NULL
  *                         (world == 1, or external collective mode)
- *   stream     cudaStream_t to run on, or NULL (the library creates one) */
+ *   stream     cudaStream_t to run on, or NULL (the library creates one)
+ *   pipeline   0: every call's work is ordered on `stream`.  1 (single GPU,
+ *              argus_route_batch_dev only): the fused tail of batch b (merge,
+ *              predictor, A5, assignment) runs on an internal high-priority
+ *              stream and overlaps the scan of batch b+1; the outputs of a call
+ *              are complete once argus_route_join / argus_sync says so.  The
+ *              prompt buffer of a call may be reused as soon as `stream` has
+ *              passed the call (the prompts are consumed by the scan part). */
 typedef struct {
   int32_t d, k, L, hidden;
   int32_t max_batch;
@@ -107,6 +114,7 @@ typedef struct {
   int32_t rank, world, device;
   const void* nccl_unique_id;
   void* stream;
+  int32_t pipeline;
 } argus_config;
 
 /* Create an ncclUniqueId (128 bytes) on rank 0; share it with the other ranks
@@ -176,7 +184,12 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
                            uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                            uint8_t* status_dev);
 
-/* Wait for the router's stream; return the deferred code of the enqueued work
+/* Make `stream` (cudaStream_t; NULL = the router's stream) wait, on the device,
+ * for all routing work enqueued so far, including pipelined tails.  No host
+ * synchronisation.  Errors: ARGUS_E_CUDA. */
+int argus_route_join(argus_router* r, void* stream);
+
+/* Wait for all of the router's work (both streams); return the deferred code of the enqueued work
  * (ARGUS_OK, ARGUS_W_OVERFLOW, ARGUS_E_INVALID) and clear it. */
 int argus_sync(argus_router* r);
 

@@ -30,7 +30,7 @@ ST_OVERFLOW, ST_NONCOMPLIANT, ST_GATED_ALL = 1, 2, 4
 SYMBOLS = (
     "argus_nccl_unique_id", "argus_route_init", "argus_cache_insert", "argus_cache_insert_dev",
     "argus_route_batch", "argus_route_batch_dev", "argus_route_partial_dev", "argus_route_finish_dev",
-    "argus_sync", "argus_quota_from_fractions", "argus_cache_size", "argus_launch_count",
+    "argus_route_join", "argus_sync", "argus_quota_from_fractions", "argus_cache_size", "argus_launch_count",
     "argus_get_stream", "argus_profile_enable", "argus_profile_read", "argus_route_destroy",
     "argus_strerror",
 )
@@ -46,7 +46,7 @@ class argus_config(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("L", C.c_int32), ("hidden", C.c_int32),
                 ("max_batch", C.c_int32), ("capacity", C.c_int64), ("delta", C.c_float),
                 ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pipeline", C.c_int32)]
 
 
 class ArgusError(RuntimeError):
@@ -70,6 +70,7 @@ def _load():
         "argus_route_batch_dev": [P, P, I32, P, P, P, P, P, P],
         "argus_route_partial_dev": [P, P, I32, P],
         "argus_route_finish_dev": [P, P, I32, I32, P, P, P, P, P, P],
+        "argus_route_join": [P, P],
         "argus_sync": [P],
         "argus_quota_from_fractions": [P, I32, I32, P],
         "argus_cache_size": [P, P],
@@ -132,7 +133,7 @@ class Router:
     """Owner of one ``argus_router*``.  Methods map 1:1 onto the C ABI."""
 
     def __init__(self, d, k, opts, W1, b1, W2, b2, capacity, max_batch, hidden=None,
-                 delta=0.9, rank=0, world=1, device=0, nccl_unique_id=None, stream=None):
+                 delta=0.9, rank=0, world=1, device=0, nccl_unique_id=None, stream=None, pipeline=False):
         L = len(opts)
         self.d, self.k, self.L = int(d), int(k), L
         W1 = np.ascontiguousarray(W1, np.float32)
@@ -149,7 +150,7 @@ class Router:
         cfg = argus_config(self.d, self.k, L, H, self.max_batch, int(capacity), float(delta),
                            int(rank), int(world), int(device),
                            C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
-                           C.c_void_p(stream) if stream else None)
+                           C.c_void_p(stream) if stream else None, int(bool(pipeline)))
         self._keep = [np.ascontiguousarray(x, np.float32) for x in (W1, b1, W2, b2)]
         h = C.c_void_p()
         _check(_lib.argus_route_init(C.byref(cfg), oa, *[_p(x) for x in self._keep], C.byref(h)),
@@ -251,6 +252,10 @@ class Router:
             _check(_lib.argus_profile_read(self._h, i, C.byref(ms), C.byref(n)), "argus_profile_read")
             out[name] = (ms.value, n.value)
         return out
+
+    def argus_route_join(self, stream=None):
+        """Make ``stream`` (raw cudaStream_t int; None = the router's) wait for all enqueued work."""
+        _check(_lib.argus_route_join(self._h, C.c_void_p(stream) if stream else None), "argus_route_join")
 
     def argus_sync(self) -> int:
         return _check(_lib.argus_sync(self._h), "argus_sync")

@@ -1,11 +1,15 @@
 // argus.cu -- host side of libargus.so: the C ABI declared in include/argus.h.
 //
-// Owns device memory, the CUDA stream, the NCCL communicator and the launch
+// Owns device memory, the CUDA streams, the NCCL communicator and the launch
 // sequence of one routing batch:
-//   K6 prep -> [NCCL broadcast of the batch when world > 1]
-//   -> K1/K2 fused scan + top-k -> K5 merge (CTA ranges)
-//   -> [NCCL all-gather of N*k keys] -> K5 merge (shards)
-//   -> K3 predictor + A5 -> K4 assignment.
+//   single GPU:  K6 prep -> K1/K2 fused scan + top-k -> fused tail (merge of the
+//                per-CTA lists, predictor, A5, assignment)
+//   world > 1:   K6 prep (rank 0) -> NCCL broadcast of the bf16 batch -> scan ->
+//                K5 local merge -> NCCL all-gather of N*k keys -> fused tail
+// Pipelined mode (cfg.pipeline): the tail of batch b runs on a high-priority
+// internal stream while batch b+1's prep + scan run on the caller's stream; the
+// per-batch buffers the two overlap on (bf16 prompts, candidate lists) are
+// double-buffered by batch parity.
 // No compute happens on the host: every step of the path is a kernel in this
 // library; the host validates arguments, moves buffers and launches.
 #include <cuda.h>
@@ -73,13 +77,19 @@ struct argus_router {
   int num_sms = 148;
   bool own_stream = false;
   cudaStream_t stream = nullptr;
+  cudaStream_t tail_stream = nullptr;  // pipelined mode: high-priority stream of the fused tail
+  bool pipe = false;
+  cudaEvent_t ev_scan[2] = {nullptr, nullptr};  // scan of the batch with parity q done
+  cudaEvent_t ev_tail[2] = {nullptr, nullptr};  // tail of the batch with parity q done
+  bool tail_inflight[2] = {false, false};
+  int64_t seq = 0;                     // pipelined batches issued
+  int cur = 0;                         // parity of the buffers the last prep/scan used
   ncclComm_t comm = nullptr;
   bool poisoned = false;
   int64_t m_global = 0;   // entries inserted (all ranks agree)
   int64_t cap_local = 0;  // rows allocated in this shard
   int64_t launches = 0;
   int32_t n_pad_max = 0;
-  int32_t p_max = 0;
   // options (device)
   int32_t* d_kskip = nullptr;
   float* d_pth = nullptr;
@@ -99,10 +109,12 @@ struct argus_router {
   float* d_invc = nullptr;
   // per-batch workspace (device)
   float* d_Xstage = nullptr;       // [max(max_batch, INSERT_CHUNK)][d] fp32 staging
-  __nv_bfloat16* d_Xb = nullptr;   // [n_pad_max][d]
+  __nv_bfloat16* d_Xb[2] = {nullptr, nullptr};  // [n_pad_max][d] per batch parity
   float* d_invq = nullptr;         // [n_pad_max]
   uint64_t* d_gthr = nullptr;      // [n_pad_max] shared per-prompt scan threshold
-  uint64_t* d_partial = nullptr;   // [p_max][max_batch][k]
+  int32_t* d_ctr = nullptr;        // [MAX_SLICES] scan work counters
+  uint64_t* d_partial[2] = {nullptr, nullptr};  // [P * N <= partial_lists][k] per batch parity
+  int64_t partial_lists = 0;
   uint64_t* d_keys = nullptr;      // [max_batch][k]
   uint64_t* d_keys_all = nullptr;  // [world][max_batch][k]
   float* d_score = nullptr;        // [max_batch][k]
@@ -121,8 +133,7 @@ struct argus_router {
   size_t outblk_bytes = 0;
   bool pending = false;            // async (_dev) work enqueued since the last argus_sync
   CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
-  CUtensorMap tmap_q;              // TMA descriptor of the bf16 prompt batch (64x128 boxes, SW128)
-  bool scan_simt = false;          // debug cross-check path (ARGUS_SCAN_SIMT=1)
+  CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   // stage profiling (argus_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -230,17 +241,18 @@ static cudaEvent_t ev_get(argus_router* r) {
 struct StageScope {
   argus_router* r;
   int stage;
+  cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
-  StageScope(argus_router* r_, int st) : r(r_), stage(st) {
+  StageScope(argus_router* r_, int st, cudaStream_t s_ = nullptr) : r(r_), stage(st), s(s_ ? s_ : r_->stream) {
     if (r->prof) {
       a = ev_get(r);
       b = ev_get(r);
-      cudaEventRecord(a, r->stream);
+      cudaEventRecord(a, s);
     }
   }
   ~StageScope() {
     if (r->prof && a && b) {
-      cudaEventRecord(b, r->stream);
+      cudaEventRecord(b, s);
       r->ev_open.push_back({stage, {a, b}});
     }
   }
@@ -249,6 +261,7 @@ struct StageScope {
 static void prof_collect(argus_router* r) {
   if (r->ev_open.empty()) return;
   cudaStreamSynchronize(r->stream);
+  if (r->tail_stream) cudaStreamSynchronize(r->tail_stream);
   for (auto& x : r->ev_open) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, x.second.first, x.second.second) == cudaSuccess) {
@@ -347,11 +360,12 @@ int argus_route_destroy(argus_router* r) {
   if (!r) return ARGUS_E_INVALID;
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  void* ptrs[] = {r->d_kskip, r->d_pth,  r->d_gate,   r->d_W1xF,  r->d_W1sT,     r->d_b1,
-                  r->d_W2,    r->d_b2, r->d_h, r->d_mlp_cnt, r->d_tail_cnt,   r->d_Cb,     r->d_invc,  r->d_Xstage,   r->d_Xb,
-                  r->d_invq,  r->d_partial, r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
-                  r->d_rhat,  r->d_pref, r->d_ccount, r->d_cmask, r->d_status,   r->d_option,
-                  r->d_order, r->d_gthr};
+  if (r->tail_stream) cudaStreamSynchronize(r->tail_stream);
+  void* ptrs[] = {r->d_kskip, r->d_pth, r->d_gate, r->d_W1xF, r->d_W1sT, r->d_b1, r->d_W2, r->d_b2, r->d_h,
+                  r->d_mlp_cnt, r->d_tail_cnt, r->d_Cb, r->d_invc, r->d_Xstage, r->d_Xb[0], r->d_Xb[1],
+                  r->d_invq, r->d_partial[0], r->d_partial[1], r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
+                  r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option, r->d_order,
+                  r->d_gthr, r->d_ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -360,6 +374,11 @@ int argus_route_destroy(argus_router* r) {
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->comm) nccl().CommDestroy(r->comm);
+  for (int q = 0; q < 2; ++q) {
+    if (r->ev_scan[q]) cudaEventDestroy(r->ev_scan[q]);
+    if (r->ev_tail[q]) cudaEventDestroy(r->ev_tail[q]);
+  }
+  if (r->tail_stream) cudaStreamDestroy(r->tail_stream);
   if (r->own_stream && r->stream) cudaStreamDestroy(r->stream);
   delete r;
   return ARGUS_OK;
@@ -414,6 +433,16 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) { delete r; return ARGUS_E_CUDA; }
     r->own_stream = true;
   }
+  r->pipe = c.pipeline != 0 && c.world == 1;
+  if (r->pipe) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    bool ok = cudaStreamCreateWithPriority(&r->tail_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
+    for (int q = 0; q < 2 && ok; ++q)
+      ok = cudaEventCreateWithFlags(&r->ev_scan[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&r->ev_tail[q], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  }
   if (c.world > 1 && c.nccl_unique_id) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_unique_id, sizeof(id));
@@ -426,7 +455,6 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   const int d = c.d, k = c.k, L = c.L, H = c.hidden, G = c.world;
   r->cap_local = (c.capacity + G - 1) / G;
   r->n_pad_max = ((c.max_batch + 127) / 128) * 128;
-  r->p_max = 2 * r->num_sms;
   const int64_t stage_rows = std::max<int64_t>(c.max_batch, INSERT_CHUNK);
   TRY_RC(dalloc(r, &r->d_kskip, L));
   TRY_RC(dalloc(r, &r->d_pth, L));
@@ -444,10 +472,15 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_Cb, (size_t)(r->cap_local + 256) * d));
   TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
   TRY_RC(dalloc(r, &r->d_Xstage, (size_t)stage_rows * d));
-  TRY_RC(dalloc(r, &r->d_Xb, (size_t)r->n_pad_max * d));
+  // P lists per prompt with P <= num_sms / slices and N <= 128 * slices
+  r->partial_lists = std::max<int64_t>((int64_t)r->num_sms * 128, c.max_batch);
+  for (int q = 0; q < 2; ++q) {
+    TRY_RC(dalloc(r, &r->d_Xb[q], (size_t)r->n_pad_max * d));
+    TRY_RC(dalloc(r, &r->d_partial[q], (size_t)r->partial_lists * k));
+  }
   TRY_RC(dalloc(r, &r->d_invq, (size_t)r->n_pad_max));
   TRY_RC(dalloc(r, &r->d_gthr, (size_t)r->n_pad_max));
-  TRY_RC(dalloc(r, &r->d_partial, (size_t)r->p_max * c.max_batch * k));
+  TRY_RC(dalloc(r, &r->d_ctr, MAX_SLICES));
   TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
@@ -465,11 +498,11 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (cudaMallocHost((void**)&r->h_outblk, r->outblk_bytes) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (!make_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d, 64) ||
-      !make_tmap(&r->tmap_q, r->d_Xb, r->n_pad_max, d, 128)) {
+      !make_tmap(&r->tmap_q[0], r->d_Xb[0], r->n_pad_max, d, 128) ||
+      !make_tmap(&r->tmap_q[1], r->d_Xb[1], r->n_pad_max, d, 128)) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
-  r->scan_simt = getenv("ARGUS_SCAN_SIMT") != nullptr;
   // zero the cache tail so TMA / vector loads past M never see garbage
   if (cudaMemsetAsync(r->d_Cb, 0, (size_t)(r->cap_local + 256) * d * sizeof(__nv_bfloat16), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
@@ -561,6 +594,8 @@ static int insert_impl(argus_router* r, const float* emb, int64_t n, int64_t* fi
   int rc = check_state(r);
   if (rc) return rc;
   if (n < 0) return ARGUS_E_INVALID;
+  rc = argus_route_join(r, nullptr);  // pipelined tails may still OR their flags
+  if (rc) return rc;
   const bool root = r->cfg.rank == 0 || !nccl_mode(r);
   if (root && n > 0 && !emb) return ARGUS_E_INVALID;
   if (r->m_global + n > r->cfg.capacity) return ARGUS_E_CAPACITY;
@@ -622,15 +657,20 @@ static int64_t local_rows(const argus_router* r) {
 
 // K6 + scan (+ K5 local merge into keys_dev when keys_dev != NULL).  *P_out receives
 // the number of per-range candidate lists left in d_partial.
-static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out);
+// q selects the double-buffered per-batch buffers (bf16 prompts, candidate lists).
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
+                        int q, bool prep_pdl = true);
 
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
   if (!keys_dev) return ARGUS_E_INVALID;
   int32_t P = 0;
-  return partial_impl(r, prompts_dev, N, keys_dev, &P);
+  int rc = argus_route_join(r, nullptr);  // pipelined tails still read the parity-0 buffers
+  if (rc) return rc;
+  return partial_impl(r, prompts_dev, N, keys_dev, &P, 0);
 }
 
-static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out) {
+static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
+                        int q, bool prep_pdl) {
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch) return ARGUS_E_INVALID;
@@ -642,18 +682,23 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
     StageScope sc(r, ARGUS_STAGE_PREP);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb, r->d_invq, r->d_gthr, r->d_flags, r->stream);
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq, r->d_gthr, r->d_ctr, r->d_flags,
+                        r->stream, prep_pdl);
     LAUNCHED(r);
   }
-  if (!root) CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
+  if (!root) {
+    CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
+    CU_TRY(r, cudaMemsetAsync(r->d_ctr, 0, sizeof(int32_t) * MAX_SLICES, r->stream));
+  }
+  r->cur = q;
   if (nccl_mode(r)) {
     NC_TRY(r, nccl().GroupStart());
-    NC_TRY(r, nccl().Broadcast(r->d_Xb, r->d_Xb, (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
+    NC_TRY(r, nccl().Broadcast(r->d_Xb[q], r->d_Xb[q], (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
     NC_TRY(r, nccl().Broadcast(r->d_invq, r->d_invq, (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
     NC_TRY(r, nccl().GroupEnd());
   }
   ScanArgs a{};
-  a.Xb = r->d_Xb;
+  a.Xb = r->d_Xb[q];
   a.inv_q = r->d_invq;
   a.Cb = r->d_Cb;
   a.inv_c = r->d_invc;
@@ -664,21 +709,21 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.k = k;
   a.rank = r->cfg.rank;
   a.world = r->cfg.world;
-  a.partial = r->d_partial;
+  a.partial = r->d_partial[q];
   a.gthr = r->d_gthr;
-  a.P = std::min(r->scan_simt ? scan_plan_ranges_simt(a.m_local, N, r->num_sms)
-                              : scan_plan_ranges(a.m_local, N, r->num_sms), r->p_max);
+  a.ctr = r->d_ctr;
+  a.P = scan_plan_ranges(a.m_local, N, r->num_sms);
+  if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
   {
     StageScope sc(r, ARGUS_STAGE_SCAN);
-    if (r->scan_simt) launch_scan_simt(a, r->stream);
-    else launch_scan(a, &r->tmap_c, &r->tmap_q, r->stream);
+    launch_scan(a, &r->tmap_c, &r->tmap_q[q], r->stream);
   }
   LAUNCHED(r);
   *P_out = a.P;
   if (keys_dev) {
     {
       StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
-      launch_merge_topk(r->d_partial, a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
+      launch_merge_topk(r->d_partial[q], a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
     }
     LAUNCHED(r);
   }
@@ -688,19 +733,19 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 // The fused tail (merge of P candidate lists per prompt, predictor, A5, assignment).
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev);
+                       uint8_t* status_dev, cudaStream_t s, bool pdl);
 
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
                            float* topk_score_dev, float* quality_dev, uint8_t* status_dev) {
   if (G < 1 || !keys_all_dev) return ARGUS_E_INVALID;
   return finish_impl(r, keys_all_dev, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                     status_dev);
+                     status_dev, r->stream, true);
 }
 
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev) {
+                       uint8_t* status_dev, cudaStream_t s, bool pdl) {
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch || P < 1 || !keys_in || !quota) return ARGUS_E_INVALID;
@@ -713,7 +758,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.P = P;
   m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
   m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
-  m.Xb = r->d_Xb;
+  m.Xb = r->d_Xb[r->cur];  // the bf16 copy of this batch made by partial_impl
   m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;
@@ -742,8 +787,8 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.status = status_dev ? status_dev : r->d_status;
   m.flags = r->d_flags;
   {
-    StageScope sc(r, ARGUS_STAGE_TAIL);
-    launch_tail(m, r->tail_smem, r->stream);
+    StageScope sc(r, ARGUS_STAGE_TAIL, s);
+    launch_tail(m, r->tail_smem, s, pdl);
   }
   LAUNCHED(r);
   return ARGUS_OK;
@@ -761,24 +806,67 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     if (quota[v] < 0) return ARGUS_E_INVALID;
   r->pending = true;
   int32_t P = 0;
-  if (!nccl_mode(r)) {  // single shard: the tail merges the per-range lists directly
-    rc = partial_impl(r, prompts_dev, N, nullptr, &P);
+  if (r->pipe) {  // prep + scan here, the tail on the tail stream (overlaps the next scan)
+    const int q = (int)(r->seq & 1);
+    // buffers q are free once the tail of batch seq-2 is done; that wait is a
+    // cross-stream edge, so prep then launches without the programmatic (PDL) relaxation
+    bool wait = false;
+    if (r->tail_inflight[q] && cudaEventQuery(r->ev_tail[q]) != cudaSuccess) {
+      (void)cudaGetLastError();  // cudaErrorNotReady is a status, not a launch error
+      wait = true;
+    }
+    if (wait) CU_TRY(r, cudaStreamWaitEvent(r->stream, r->ev_tail[q], 0));
+    rc = partial_impl(r, prompts_dev, N, nullptr, &P, q, !wait);
     if (rc) return rc;
-    return finish_impl(r, r->d_partial, P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                       status_dev);
+    CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->stream));
+    CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_scan[q], 0));
+    rc = finish_impl(r, r->d_partial[q], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
+                     status_dev, r->tail_stream, false);
+    if (rc) return rc;
+    CU_TRY(r, cudaEventRecord(r->ev_tail[q], r->tail_stream));
+    r->tail_inflight[q] = true;
+    r->seq++;
+    return ARGUS_OK;
   }
-  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P);
+  if (!nccl_mode(r)) {  // single shard: the tail merges the per-CTA lists directly
+    rc = partial_impl(r, prompts_dev, N, nullptr, &P, 0);
+    if (rc) return rc;
+    return finish_impl(r, r->d_partial[0], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
+                       status_dev, r->stream, true);
+  }
+  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P, 0);
   if (rc) return rc;
   // C-2: N*k candidate keys from every shard
   NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
   return finish_impl(r, r->d_keys_all, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
-                     quality_dev, status_dev);
+                     quality_dev, status_dev, r->stream, true);
+}
+
+int argus_route_join(argus_router* r, void* stream) {
+  if (!r) return ARGUS_E_INVALID;
+  if (r->poisoned) return ARGUS_E_STATE;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : r->stream;
+  for (int q = 0; q < 2; ++q)
+    if (r->tail_inflight[q]) {
+      CU_TRY(r, cudaStreamWaitEvent(s, r->ev_tail[q], 0));
+      if (s == r->stream) r->tail_inflight[q] = false;  // ordered behind it from now on
+    }
+  if (s != r->stream) {  // and behind everything on the router's own stream
+    cudaEvent_t e = ev_get(r);
+    CU_TRY(r, cudaEventRecord(e, r->stream));
+    CU_TRY(r, cudaStreamWaitEvent(s, e, 0));
+    r->ev_pool.push_back(e);  // reuse is safe: a wait binds to the record issued before it
+  }
+  return ARGUS_OK;
 }
 
 int argus_sync(argus_router* r) {
   int rc = check_state(r);
   if (rc) return rc;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = argus_route_join(r, nullptr);
+  if (rc) return rc;
   CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
   CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
   CU_TRY(r, cudaStreamSynchronize(r->stream));
@@ -816,6 +904,8 @@ int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const in
   rc = argus_route_batch_dev(r, r->d_Xstage, N, quota, reinterpret_cast<int32_t*>(D + o_opt),
                              reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
                              reinterpret_cast<float*>(D + o_rh), D + o_st);
+  if (rc) return rc;
+  rc = argus_route_join(r, nullptr);
   if (rc) return rc;
   CU_TRY(r, cudaMemcpyAsync(r->h_outblk, D, o_end, cudaMemcpyDeviceToHost, r->stream));
   CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));

@@ -52,10 +52,11 @@ __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t
 
 __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, int d,
                                __nv_bfloat16* __restrict__ Xb, float* __restrict__ inv_q,
-                               uint64_t* __restrict__ gthr, uint32_t* flags) {
+                               uint64_t* __restrict__ gthr, int32_t* __restrict__ ctr, uint32_t* flags) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   pdl_wait();  // the previous batch's kernels may still read Xb / inv_q
+  if (blockIdx.x == 0 && threadIdx.x < MAX_SLICES) ctr[threadIdx.x] = 0;  // scan work counters
   if (warp >= n_pad) return;
   if (lane == 0) gthr[warp] = 0;  // the scan's shared per-prompt threshold starts empty
   if (warp >= N) {  // zero padding rows: score 0, never reported
@@ -86,10 +87,10 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 }
 
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
-                         float* inv_q, uint64_t* gthr, uint32_t* flags, cudaStream_t s) {
+                         float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s, bool pdl) {
   const int threads = 256;
   int blocks = (n_pad * 32 + threads - 1) / threads;
-  launch_pdl(k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, flags);
+  launch_pdl_opt(pdl, k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, ctr, flags);
 }
 
 }  // namespace argus

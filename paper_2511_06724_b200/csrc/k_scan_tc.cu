@@ -5,28 +5,25 @@
 //   S[i, j] = (<Xb_i, Cb_j> * inv_c[j]) * inv_q[i]   bf16 x bf16 -> fp32 accumulate
 //   top-k per prompt i over (S desc, global id asc); S never reaches HBM.
 //
-// B200 design (DESIGN.md §"K1"):
-//   * one CTA per SM (persistent); CTA = one 128-prompt slice x one contiguous
-//     range of cache tiles; all CTAs of a range run concurrently, so the cache
-//     streams from HBM once and slices > 1 re-hit it in L2;
+// B200 design (DESIGN.md §7 "K1"):
+//   * one CTA per SM; CTA = one 128-prompt slice; the cache tiles of a slice are
+//     handed out dynamically in chunks of CHUNK tiles (one atomic per chunk, fetched
+//     a chunk ahead), so CTAs that start late (SMs still busy with the previous
+//     batch's tail kernel) just take fewer chunks; CTAs of all slices sweep the
+//     cache in the same order, so slices > 1 re-hit each tile in L2;
 //   * the prompt slice is the UMMA A operand and lives in TMEM for the whole
 //     kernel (128 lanes x d/2 columns, loaded once with tcgen05.st);
-//   * cache tiles of 64 rows are the B operand: TMA (128-byte swizzle) streams
-//     64x64 bf16 boxes into two tile buffers (d/64 boxes each, one mbarrier per
-//     box so the MMAs start as soon as the first box lands);
+//   * cache tiles of 64 rows are the B operand: TMA (128-byte swizzle, L2
+//     evict-first) streams 64x64 bf16 boxes through a ring of 4 half-tile slots;
 //   * tcgen05.mma.cta_group::1.kind::f16, M=128 (prompts) x N=64 (cache rows) x
-//     K=16, issued by one thread into one of two TMEM accumulators
-//     (double-buffered, so the epilogue of tile t overlaps the MMAs of t+1);
-//     ONE tcgen05.commit per tile frees both the tile buffer and signals the
-//     accumulator (measured: a commit costs ~250 issue cycles, an N=64 MMA ~45,
-//     so per-k-block commits made the issue loop the bottleneck);
-//   * the prompt slice reaches TMEM through the tile buffers (one TMA burst, then
-//     shared memory -> registers -> tcgen05.st), not through dependent global loads;
-//   * epilogue: 4 warps, TMEM lane = prompt, so each thread owns ONE prompt and
-//     keeps its top-k in registers behind a float threshold: per score two
-//     FMULs, one compare; inserts are rare (~k ln(M/k) per prompt).
+//     K=16, issued warp-uniformly (elect.sync inside the asm) into one of two TMEM
+//     accumulators, one tcgen05.commit per half tile (a commit costs ~250 issue
+//     cycles, an N=64 MMA ~32);
+//   * epilogue: 8 warps, TMEM lane = prompt, each thread owns one prompt and one
+//     32-column half of every tile and keeps its top-k in registers behind a float
+//     threshold shared (monotonically) with the other lists of the same prompt.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 3 = idle,
-// 4..7 = Q loader + epilogue.
+// 4..11 = Q loader + epilogue.
 #include "common.cuh"
 #include "kernels.h"
 #include "tc.cuh"
@@ -52,6 +49,7 @@ constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int INV_SLOTS = 8;
+constexpr int CHUNK = 4;                    // tiles per dynamically scheduled work unit
 constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 16 x 32 fp32 slow-path scratch
 constexpr size_t SMEM_BYTES = (size_t)RING_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -64,7 +62,9 @@ struct ScanSmem {  // placed after the ring
   uint64_t tempty[2];           // epilogue has read accumulator b
   uint64_t qfull;               // prompt slice landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
-  uint64_t invfull[INV_SLOTS];  // inv_c slot l % 8 landed (cannot lap, see the epilogue)
+  uint64_t invfull[INV_SLOTS];  // inv_c slot l % 8 landed (cannot lap, see the epilogue); also
+                                // publishes tile_id[l % 8] (-1 = no more tiles)
+  int64_t tile_id[INV_SLOTS];   // cache tile of the CTA's l-th tile
   uint32_t tmem_base;
   uint32_t pad_[3];
   float invc[INV_SLOTS][TN];    // inverse cache-row norms of tile l in slot l % 8 (bulk copy)
@@ -131,16 +131,14 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
 template <int KMAX>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
-              int slices, int ranges, int64_t n_tiles) {
+              int slices, int64_t n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)RING_BYTES);
   const uint32_t ring_s = tc::smem_u32(ring);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x % slices;
-  const int range = blockIdx.x / slices;
-  const int64_t t_begin = n_tiles * range / ranges;
-  const int64_t t_end = n_tiles * (range + 1) / ranges;
+  const int range = blockIdx.x / slices;  // index of this CTA's candidate list
   const int KB = a.d / KBLK;
 
   if (warp == 0 && lane == 0) {
@@ -179,25 +177,38 @@ __global__ void __launch_bounds__(THREADS, 1)
       // other slices of the range re-read each tile from L2 within microseconds
       const uint64_t pol = tc::policy_evict_first();
       const int kb_half[2] = {(KB + 1) / 2, KB / 2};
+      int* ctr = a.ctr + slice;
       int64_t l = 0;
-      for (int64_t t = t_begin; t < t_end; ++t, ++l) {
-        for (int hh = 0; hh < 2; ++hh) {
-          const int64_t u = 2 * l + hh;  // half-tile sequence number
-          const int sl = (int)(u & (NSLOT - 1));
-          tc::mbar_wait(tc::smem_u32(&sm->empty[sl]), (uint32_t)(((u >> 2) & 1) ^ 1));
-          const uint32_t fb = tc::smem_u32(&sm->full[sl]);
-          tc::mbar_arrive_expect_tx(fb, (uint32_t)(kb_half[hh] * BOX_BYTES));
-          if (hh == 0) {  // the tile's inverse norms (rows past capacity read zeros)
-            const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
-            tc::mbar_arrive_expect_tx(ib, TN * 4);
-            tc::bulk_load_hint(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib, pol);
+      int64_t c = atomicAdd(ctr, 1);
+      for (;;) {
+        const int64_t t0 = c * CHUNK;
+        if (t0 >= n_tiles) break;
+        c = atomicAdd(ctr, 1);  // next chunk: the latency overlaps this chunk's loads
+        const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
+        for (int64_t t = t0; t < t1; ++t, ++l) {
+          for (int hh = 0; hh < 2; ++hh) {
+            const int64_t u = 2 * l + hh;  // half-tile sequence number
+            const int sl = (int)(u & (NSLOT - 1));
+            tc::mbar_wait(tc::smem_u32(&sm->empty[sl]), (uint32_t)(((u >> 2) & 1) ^ 1));
+            const uint32_t fb = tc::smem_u32(&sm->full[sl]);
+            tc::mbar_arrive_expect_tx(fb, (uint32_t)(kb_half[hh] * BOX_BYTES));
+            if (hh == 0) {  // the tile's id and inverse norms (rows past capacity read zeros)
+              sm->tile_id[l & (INV_SLOTS - 1)] = t;
+              const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
+              tc::mbar_arrive_expect_tx(ib, TN * 4);
+              tc::bulk_load_hint(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib, pol);
+            }
+            const int kb0 = hh ? kb_half[0] : 0;
+            for (int j = 0; j < kb_half[hh]; ++j)
+              tc::tma_load_2d_hint(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb,
+                                   (kb0 + j) * KBLK, (int32_t)(t * TN), pol);
           }
-          const int kb0 = hh ? kb_half[0] : 0;
-          for (int j = 0; j < kb_half[hh]; ++j)
-            tc::tma_load_2d_hint(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb, (kb0 + j) * KBLK,
-                                 (int32_t)(t * TN), pol);
         }
       }
+      // end marker in the next tile slot (same reuse rule as a real tile)
+      tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l) & (NSLOT - 1)]), (uint32_t)((((2 * l) >> 2) & 1) ^ 1));
+      sm->tile_id[l & (INV_SLOTS - 1)] = -1;
+      tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (warp-uniform loop, elect.sync issue)
@@ -206,8 +217,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::fence_after();
     const int kb_half0 = (KB + 1) / 2;
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
-    int64_t l = 0;
-    for (int64_t t = t_begin; t < t_end; ++t, ++l) {
+    for (int64_t l = 0;; ++l) {
+      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
+      if (sm->tile_id[l & (INV_SLOTS - 1)] < 0) break;
       const int b = (int)(l & 1);
       tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
       tc::fence_after();
@@ -275,16 +287,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* gthr_p = a.gthr + p;
     uint64_t published = 0;
     uint64_t gk = active ? __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p)) : 0;
-    int64_t l = 0;
-    for (int64_t t = t_begin; t < t_end; ++t, ++l) {
+    for (int64_t l = 0;; ++l) {
       __syncwarp();
+      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
+      const int64_t t = sm->tile_id[l & (INV_SLOTS - 1)];
+      if (t < 0) break;
       if (gk != 0) thr = fmaxf(thr, key_score(gk));
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
       // the tile's second half-slot (2l+1) % 4 completing means all its MMAs are done;
       // it cannot lap: reuse by tile l+2 needs this warp's release of tile l
       tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l + 1) & (NSLOT - 1)]), (uint32_t)((l >> 1) & 1));
-      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       tc::fence_after();
       uint32_t v[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + h * 32, v);
@@ -340,16 +353,15 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
   const int slices = (N + TM - 1) / TM;
   int ranges = num_sms / slices;
   if (ranges < 1) ranges = 1;
-  const int64_t n_tiles = (m_local + TN - 1) / TN;
-  if (ranges > n_tiles) ranges = (int)(n_tiles > 0 ? n_tiles : 1);
-  return ranges;  // one partial list per (range, prompt)
+  const int64_t n_chunks = ((m_local + TN - 1) / TN + CHUNK - 1) / CHUNK;
+  if (ranges > n_chunks) ranges = (int)(n_chunks > 0 ? n_chunks : 1);
+  return ranges;  // CTAs per slice = candidate lists per prompt
 }
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s) {
   const int slices = (a.N + TM - 1) / TM;
-  const int ranges = a.P;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   static bool attr = false;
   if (!attr) {
@@ -357,11 +369,11 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
     cudaFuncSetAttribute(k_scan_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     attr = true;
   }
-  const dim3 grid(slices * ranges);
+  const dim3 grid(slices * a.P);
   if (a.k <= 4)
-    launch_pdl(k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, ranges, n_tiles);
+    launch_pdl(k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles);
   else
-    launch_pdl(k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, ranges, n_tiles);
+    launch_pdl(k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles);
 }
 
 }  // namespace argus

@@ -482,14 +482,14 @@ void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStr
   k_prep_w1_frag<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(w1, d, k, H, reinterpret_cast<uint2*>(Wf));
 }
 
-void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s) {
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl) {
   static size_t attr_set = 0;
   if (smem > attr_set) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = smem;
   }
   const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
-  launch_pdl(k_tail, grid, dim3(TT), smem, s, a);
+  launch_pdl_opt(pdl, k_tail, grid, dim3(TT), smem, s, a);
 }
 
 }  // namespace argus

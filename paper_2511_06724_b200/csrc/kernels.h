@@ -10,8 +10,8 @@ namespace argus {
 
 // Launch with programmatic stream serialization (PDL); see common.cuh.
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args&&... args) {
+inline cudaError_t launch_pdl_opt(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -21,8 +21,13 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  return launch_pdl_opt(true, kern, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 // error flags written by kernels into a device word (bitwise OR)
@@ -39,7 +44,9 @@ struct ScanArgs {
   uint64_t* partial;         // [P][N][k] per-CTA-range candidates
   int32_t P;                 // number of cache ranges (filled by the planner)
   uint64_t* gthr;            // [n_pad] per-prompt shared top-k threshold key (zeroed by K6)
+  int32_t* ctr;              // [MAX_SLICES] per-slice tile-chunk work counters (zeroed by K6)
 };
+constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts
 
 // K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
 // g % world == rank go to slot g / world.
@@ -49,16 +56,14 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 
 // K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
-                         float* inv_q, uint64_t* gthr, uint32_t* flags, cudaStream_t s);
+                         float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s,
+                         bool pdl = true);
 
 // K1+K2: fused tcgen05 scan + per-range top-k -> partial [P][N][k].
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
 int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);
 bool scan_supported(int d);
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q, cudaStream_t s);
-// SIMT reference-quality scan (debug cross-check only, ARGUS_SCAN_SIMT=1)
-int scan_plan_ranges_simt(int64_t m_local, int32_t N, int num_sms);
-void launch_scan_simt(const ScanArgs& a, cudaStream_t s);
 
 // K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
 // decoding ids / scores.
@@ -98,7 +103,9 @@ struct TailArgs {
   uint32_t* flags;
 };
 // K3+K4 (+K5 on one GPU): merge, predictor, A5 and the assignment in one launch.
-void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s);
+// pdl = false when the tail's producer is on another stream (pipelined mode):
+// griddepcontrol.wait only orders against the previous kernel of the same stream.
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl);
 size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max);
 // init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
 void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);

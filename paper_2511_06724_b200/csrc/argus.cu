@@ -6,10 +6,11 @@
 //                per-CTA lists, predictor, A5, assignment)
 //   world > 1:   K6 prep (rank 0) -> NCCL broadcast of the bf16 batch -> scan ->
 //                K5 local merge -> NCCL all-gather of N*k keys -> fused tail
-// Pipelined mode (cfg.pipeline): the tail of batch b runs on a high-priority
-// internal stream while batch b+1's prep + scan run on the caller's stream; the
-// per-batch buffers the two overlap on (bf16 prompts, candidate lists) are
-// double-buffered by batch parity.
+// Pipelined mode (cfg.pipeline): three internal streams.  prep(b) (high priority)
+// runs as soon as the caller's stream has the prompts, concurrently with scan(b-1);
+// the scan stream runs the scans back to back; the tail of batch b (high priority)
+// overlaps scan(b+1).  All per-batch buffers are double-buffered by batch parity q;
+// prep(b) reuses parity q once tail(b-2) (hence scan(b-2)) is done.
 // No compute happens on the host: every step of the path is a kernel in this
 // library; the host validates arguments, moves buffers and launches.
 #include <cuda.h>
@@ -77,8 +78,12 @@ struct argus_router {
   int num_sms = 148;
   bool own_stream = false;
   cudaStream_t stream = nullptr;
-  cudaStream_t tail_stream = nullptr;  // pipelined mode: high-priority stream of the fused tail
+  cudaStream_t prep_stream = nullptr;  // pipelined mode: K6 (high priority)
+  cudaStream_t scan_stream = nullptr;  // pipelined mode: the scans, back to back
+  cudaStream_t tail_stream = nullptr;  // pipelined mode: the fused tails (high priority)
   bool pipe = false;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr};    // caller's stream reached the call of parity q
+  cudaEvent_t ev_prep[2] = {nullptr, nullptr};  // prep of the batch with parity q done
   cudaEvent_t ev_scan[2] = {nullptr, nullptr};  // scan of the batch with parity q done
   cudaEvent_t ev_tail[2] = {nullptr, nullptr};  // tail of the batch with parity q done
   bool tail_inflight[2] = {false, false};
@@ -110,9 +115,9 @@ struct argus_router {
   // per-batch workspace (device)
   float* d_Xstage = nullptr;       // [max(max_batch, INSERT_CHUNK)][d] fp32 staging
   __nv_bfloat16* d_Xb[2] = {nullptr, nullptr};  // [n_pad_max][d] per batch parity
-  float* d_invq = nullptr;         // [n_pad_max]
-  uint64_t* d_gthr = nullptr;      // [n_pad_max] shared per-prompt scan threshold
-  int32_t* d_ctr = nullptr;        // [MAX_SLICES] scan work counters
+  float* d_invq[2] = {nullptr, nullptr};     // [n_pad_max] per batch parity
+  uint64_t* d_gthr[2] = {nullptr, nullptr};  // [n_pad_max] shared per-prompt scan threshold
+  int32_t* d_ctr[2] = {nullptr, nullptr};    // [MAX_SLICES] scan work counters
   uint64_t* d_partial[2] = {nullptr, nullptr};  // [P * N <= partial_lists][k] per batch parity
   int64_t partial_lists = 0;
   uint64_t* d_keys = nullptr;      // [max_batch][k]
@@ -261,7 +266,8 @@ struct StageScope {
 static void prof_collect(argus_router* r) {
   if (r->ev_open.empty()) return;
   cudaStreamSynchronize(r->stream);
-  if (r->tail_stream) cudaStreamSynchronize(r->tail_stream);
+  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream})
+    if (s) cudaStreamSynchronize(s);
   for (auto& x : r->ev_open) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, x.second.first, x.second.second) == cudaSuccess) {
@@ -360,12 +366,13 @@ int argus_route_destroy(argus_router* r) {
   if (!r) return ARGUS_E_INVALID;
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  if (r->tail_stream) cudaStreamSynchronize(r->tail_stream);
+  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream})
+    if (s) cudaStreamSynchronize(s);
   void* ptrs[] = {r->d_kskip, r->d_pth, r->d_gate, r->d_W1xF, r->d_W1sT, r->d_b1, r->d_W2, r->d_b2, r->d_h,
                   r->d_mlp_cnt, r->d_tail_cnt, r->d_Cb, r->d_invc, r->d_Xstage, r->d_Xb[0], r->d_Xb[1],
-                  r->d_invq, r->d_partial[0], r->d_partial[1], r->d_keys, r->d_keys_all, r->d_score, r->d_idx,
-                  r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option, r->d_order,
-                  r->d_gthr, r->d_ctr};
+                  r->d_invq[0], r->d_invq[1], r->d_partial[0], r->d_partial[1], r->d_keys, r->d_keys_all,
+                  r->d_score, r->d_idx, r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option,
+                  r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -374,11 +381,11 @@ int argus_route_destroy(argus_router* r) {
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->comm) nccl().CommDestroy(r->comm);
-  for (int q = 0; q < 2; ++q) {
-    if (r->ev_scan[q]) cudaEventDestroy(r->ev_scan[q]);
-    if (r->ev_tail[q]) cudaEventDestroy(r->ev_tail[q]);
-  }
-  if (r->tail_stream) cudaStreamDestroy(r->tail_stream);
+  for (int q = 0; q < 2; ++q)
+    for (cudaEvent_t e : {r->ev_in[q], r->ev_prep[q], r->ev_scan[q], r->ev_tail[q]})
+      if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream})
+    if (s) cudaStreamDestroy(s);
   if (r->own_stream && r->stream) cudaStreamDestroy(r->stream);
   delete r;
   return ARGUS_OK;
@@ -437,9 +444,13 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (r->pipe) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    bool ok = cudaStreamCreateWithPriority(&r->tail_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
+    bool ok = cudaStreamCreateWithPriority(&r->prep_stream, cudaStreamNonBlocking, hi) == cudaSuccess &&
+              cudaStreamCreateWithPriority(&r->scan_stream, cudaStreamNonBlocking, lo) == cudaSuccess &&
+              cudaStreamCreateWithPriority(&r->tail_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
     for (int q = 0; q < 2 && ok; ++q)
-      ok = cudaEventCreateWithFlags(&r->ev_scan[q], cudaEventDisableTiming) == cudaSuccess &&
+      ok = cudaEventCreateWithFlags(&r->ev_in[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&r->ev_prep[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&r->ev_scan[q], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&r->ev_tail[q], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   }
@@ -478,9 +489,11 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     TRY_RC(dalloc(r, &r->d_Xb[q], (size_t)r->n_pad_max * d));
     TRY_RC(dalloc(r, &r->d_partial[q], (size_t)r->partial_lists * k));
   }
-  TRY_RC(dalloc(r, &r->d_invq, (size_t)r->n_pad_max));
-  TRY_RC(dalloc(r, &r->d_gthr, (size_t)r->n_pad_max));
-  TRY_RC(dalloc(r, &r->d_ctr, MAX_SLICES));
+  for (int q = 0; q < 2; ++q) {
+    TRY_RC(dalloc(r, &r->d_invq[q], (size_t)r->n_pad_max));
+    TRY_RC(dalloc(r, &r->d_gthr[q], (size_t)r->n_pad_max));
+    TRY_RC(dalloc(r, &r->d_ctr[q], MAX_SLICES));
+  }
   TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
@@ -659,7 +672,7 @@ static int64_t local_rows(const argus_router* r) {
 // the number of per-range candidate lists left in d_partial.
 // q selects the double-buffered per-batch buffers (bf16 prompts, candidate lists).
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
-                        int q, bool prep_pdl = true);
+                        int q, cudaStream_t s_prep = nullptr, cudaStream_t s_scan = nullptr);
 
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
   if (!keys_dev) return ARGUS_E_INVALID;
@@ -669,8 +682,13 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
   return partial_impl(r, prompts_dev, N, keys_dev, &P, 0);
 }
 
+// With s_prep / s_scan (pipelined mode) prep and scan go to those streams, without
+// the programmatic (PDL) relaxation, and the caller inserts the events between them.
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
-                        int q, bool prep_pdl) {
+                        int q, cudaStream_t s_prep, cudaStream_t s_scan) {
+  const bool pipelined = s_prep != nullptr;
+  if (!s_prep) s_prep = r->stream;
+  if (!s_scan) s_scan = r->stream;
   int rc = check_state(r);
   if (rc) return rc;
   if (N < 1 || N > r->cfg.max_batch) return ARGUS_E_INVALID;
@@ -681,25 +699,30 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   const int n_pad = ((N + 127) / 128) * 128;
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
-    StageScope sc(r, ARGUS_STAGE_PREP);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq, r->d_gthr, r->d_ctr, r->d_flags,
-                        r->stream, prep_pdl);
+    StageScope sc(r, ARGUS_STAGE_PREP, s_prep);
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q], r->d_flags,
+                        s_prep, !pipelined);
     LAUNCHED(r);
   }
   if (!root) {
-    CU_TRY(r, cudaMemsetAsync(r->d_gthr, 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
-    CU_TRY(r, cudaMemsetAsync(r->d_ctr, 0, sizeof(int32_t) * MAX_SLICES, r->stream));
+    CU_TRY(r, cudaMemsetAsync(r->d_gthr[q], 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
+    CU_TRY(r, cudaMemsetAsync(r->d_ctr[q], 0, sizeof(int32_t) * MAX_SLICES, r->stream));
+  }
+  if (pipelined) {
+    CU_TRY(r, cudaEventRecord(r->ev_prep[q], s_prep));
+    CU_TRY(r, cudaStreamWaitEvent(s_scan, r->ev_prep[q], 0));
+    CU_TRY(r, cudaStreamWaitEvent(r->stream, r->ev_prep[q], 0));  // the prompt buffer is consumed
   }
   r->cur = q;
   if (nccl_mode(r)) {
     NC_TRY(r, nccl().GroupStart());
     NC_TRY(r, nccl().Broadcast(r->d_Xb[q], r->d_Xb[q], (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
-    NC_TRY(r, nccl().Broadcast(r->d_invq, r->d_invq, (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
+    NC_TRY(r, nccl().Broadcast(r->d_invq[q], r->d_invq[q], (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
     NC_TRY(r, nccl().GroupEnd());
   }
   ScanArgs a{};
   a.Xb = r->d_Xb[q];
-  a.inv_q = r->d_invq;
+  a.inv_q = r->d_invq[q];
   a.Cb = r->d_Cb;
   a.inv_c = r->d_invc;
   a.m_local = local_rows(r);
@@ -710,13 +733,13 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.rank = r->cfg.rank;
   a.world = r->cfg.world;
   a.partial = r->d_partial[q];
-  a.gthr = r->d_gthr;
-  a.ctr = r->d_ctr;
+  a.gthr = r->d_gthr[q];
+  a.ctr = r->d_ctr[q];
   a.P = scan_plan_ranges(a.m_local, N, r->num_sms);
   if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
   {
-    StageScope sc(r, ARGUS_STAGE_SCAN);
-    launch_scan(a, &r->tmap_c, &r->tmap_q[q], r->stream);
+    StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
+    launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
   }
   LAUNCHED(r);
   *P_out = a.P;
@@ -806,19 +829,14 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     if (quota[v] < 0) return ARGUS_E_INVALID;
   r->pending = true;
   int32_t P = 0;
-  if (r->pipe) {  // prep + scan here, the tail on the tail stream (overlaps the next scan)
+  if (r->pipe) {  // prep / scan / tail on the internal streams (see the file header)
     const int q = (int)(r->seq & 1);
-    // buffers q are free once the tail of batch seq-2 is done; that wait is a
-    // cross-stream edge, so prep then launches without the programmatic (PDL) relaxation
-    bool wait = false;
-    if (r->tail_inflight[q] && cudaEventQuery(r->ev_tail[q]) != cudaSuccess) {
-      (void)cudaGetLastError();  // cudaErrorNotReady is a status, not a launch error
-      wait = true;
-    }
-    if (wait) CU_TRY(r, cudaStreamWaitEvent(r->stream, r->ev_tail[q], 0));
-    rc = partial_impl(r, prompts_dev, N, nullptr, &P, q, !wait);
+    CU_TRY(r, cudaEventRecord(r->ev_in[q], r->stream));  // prompts (and earlier inserts) are ready
+    CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_in[q], 0));
+    if (r->tail_inflight[q]) CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_tail[q], 0));  // parity q free
+    rc = partial_impl(r, prompts_dev, N, nullptr, &P, q, r->prep_stream, r->scan_stream);
     if (rc) return rc;
-    CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->stream));
+    CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->scan_stream));
     CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_scan[q], 0));
     rc = finish_impl(r, r->d_partial[q], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
                      status_dev, r->tail_stream, false);

@@ -24,6 +24,8 @@
 //     threshold shared (monotonically) with the other lists of the same prompt.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 3 = idle,
 // 4..11 = Q loader + epilogue.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc.cuh"
@@ -131,7 +133,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
 template <int KMAX>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
-              int slices, int64_t n_tiles) {
+              int slices, int64_t n_tiles, int l2mode) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)RING_BYTES);
@@ -174,8 +176,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tma_load_2d(ring_s + (uint32_t)(kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
       tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // ring free again
       // one slice streams the cache exactly once: evict-first; with several slices the
-      // other slices of the range re-read each tile from L2 within microseconds
-      const uint64_t pol = tc::policy_evict_first();
+      // other slices re-read each tile from L2 shortly after the first reader
+      const uint64_t pol = l2mode == 0 ? tc::policy_evict_first()
+                                       : (l2mode == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
       const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int* ctr = a.ctr + slice;
       int64_t l = 0;
@@ -360,7 +363,7 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
-void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s) {
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s, bool pdl) {
   const int slices = (a.N + TM - 1) / TM;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   static bool attr = false;
@@ -370,10 +373,18 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
     attr = true;
   }
   const dim3 grid(slices * a.P);
+  // L2 policy of the cache stream: evict-first for one slice, normal LRU when
+  // several slices re-read each tile (ARGUS_SCAN_L2=0/1/2 overrides, experiments)
+  static int l2env = -2;
+  if (l2env == -2) {
+    const char* e = getenv("ARGUS_SCAN_L2");
+    l2env = e ? atoi(e) : -1;
+  }
+  const int l2mode = l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1);
   if (a.k <= 4)
-    launch_pdl(k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles);
+    launch_pdl_opt(pdl, k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
   else
-    launch_pdl(k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles);
+    launch_pdl_opt(pdl, k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
 }
 
 }  // namespace argus

@@ -63,7 +63,8 @@ void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
 int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);
 bool scan_supported(int d);
-void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q, cudaStream_t s);
+void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q, cudaStream_t s,
+                 bool pdl = true);
 
 // K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
 // decoding ids / scores.

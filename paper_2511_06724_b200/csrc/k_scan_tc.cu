@@ -177,16 +177,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // ring free again
       // one slice streams the cache exactly once: evict-first; with several slices the
       // other slices re-read each tile from L2 shortly after the first reader
-      const uint64_t pol = l2mode == 0 ? tc::policy_evict_first()
-                                       : (l2mode == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
+      const int l2m = l2mode & 15;
+      const uint64_t pol = l2m == 0 ? tc::policy_evict_first()
+                                    : (l2m == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
       const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int* ctr = a.ctr + slice;
       int64_t l = 0;
-      int64_t c = atomicAdd(ctr, 1);
+      // static split (diagnostics): CTA `range` takes chunks [c_lo, c_hi) in order
+      const int64_t n_chunks = (n_tiles + CHUNK - 1) / CHUNK;
+      const int64_t c_lo = n_chunks * range / (gridDim.x / slices), c_hi = n_chunks * (range + 1) / (gridDim.x / slices);
+      int64_t c = l2mode >= 16 ? c_lo : atomicAdd(ctr, 1);
       for (;;) {
         const int64_t t0 = c * CHUNK;
-        if (t0 >= n_tiles) break;
-        c = atomicAdd(ctr, 1);  // next chunk: the latency overlaps this chunk's loads
+        if (t0 >= n_tiles || (l2mode >= 16 && c >= c_hi)) break;
+        c = l2mode >= 16 ? c + 1 : atomicAdd(ctr, 1);  // next chunk: the latency overlaps this chunk's loads
         const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
         for (int64_t t = t0; t < t1; ++t, ++l) {
           for (int hh = 0; hh < 2; ++hh) {
@@ -208,19 +212,28 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      // end marker in the next tile slot (same reuse rule as a real tile)
-      tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l) & (NSLOT - 1)]), (uint32_t)((((2 * l) >> 2) & 1) ^ 1));
-      sm->tile_id[l & (INV_SLOTS - 1)] = -1;
-      tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
+      // end markers in the next two tile slots (one per MMA issuer; same reuse rule as
+      // a real tile)
+      for (int e = 0; e < 2; ++e, ++l) {
+        tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l) & (NSLOT - 1)]), (uint32_t)((((2 * l) >> 2) & 1) ^ 1));
+        sm->tile_id[l & (INV_SLOTS - 1)] = -1;
+        tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
+      }
     }
-  } else if (warp == 1) {
-    // ======================= MMA issuer (warp-uniform loop, elect.sync issue)
+  } else if (warp == 1 || (warp == 3 && !(l2mode & 32))) {
+    // ======================= MMA issuers: warp 1 takes the even tiles (half-slots 0,1,
+    // accumulator 0), warp 3 the odd ones (half-slots 2,3, accumulator 1).  One warp's
+    // issue loop (~14 instructions and a dependent R2UR chain per MMA, plus the
+    // commits) is slower than the 32 cycles an M=128 N=64 K=16 MMA executes in; two
+    // interleaved issuers keep the tensor pipe fed.  tcgen05.commit tracks the MMAs
+    // of the committing thread only, so the two barrier sets stay independent.
     constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
     tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
     tc::fence_after();
     const int kb_half0 = (KB + 1) / 2;
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
-    for (int64_t l = 0;; ++l) {
+    const int lstep = (l2mode & 32) ? 1 : 2;
+    for (int64_t l = warp == 1 ? 0 : 1;; l += lstep) {
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       if (sm->tile_id[l & (INV_SLOTS - 1)] < 0) break;
       const int b = (int)(l & 1);
@@ -380,7 +393,8 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
     const char* e = getenv("ARGUS_SCAN_L2");
     l2env = e ? atoi(e) : -1;
   }
-  const int l2mode = l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1);
+  static int stat = (getenv("ARGUS_SCAN_STATIC") ? 16 : 0) | (getenv("ARGUS_SCAN_1MMA") ? 32 : 0);
+  const int l2mode = (l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1)) | stat;
   if (a.k <= 4)
     launch_pdl_opt(pdl, k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
   else

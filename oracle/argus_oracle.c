@@ -101,30 +101,49 @@ static int better(double s, uint32_t g, double s2, uint32_t g2) {
 int orc_scan_topk(const float* X, int32_t N, const float* C, int64_t M, int32_t d, int32_t k,
                   const uint32_t* ids, int nthreads, double* topk_score, uint32_t* topk_idx) {
     if (N < 0 || M < 0 || d <= 0 || k <= 0) return ORC_EINVAL;
-    /* O2: norms of the bf16 cache rows */
-    double* nc = (double*)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1));
-    if (!nc) return ORC_EINVAL;
-    int bad = 0;
-    for (int64_t j = 0; j < M; ++j) {
-        nc[j] = norm_bf16(C + j * d, d);
-        if (!(nc[j] > 0.0) || !isfinite(nc[j])) bad = 1;
-    }
-    if (bad) { free(nc); return ORC_EINVAL; }
-    int badq = 0;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    /* O1 once per input: the bf16 values of X and C (exactly representable in float,
+     * so this copy is lossless); the products and sums below are the same fp64
+     * operations in the same order as dot_bf16 on the raw rows. */
+    float* Cb = (float*)malloc(sizeof(float) * (size_t)(M > 0 ? M : 1) * (size_t)d);
+    float* Xb = (float*)malloc(sizeof(float) * (size_t)(N > 0 ? N : 1) * (size_t)d);
+    double* nc = (double*)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1));
+    if (!Cb || !Xb || !nc) { free(Cb); free(Xb); free(nc); return ORC_EINVAL; }
+    int bad = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) reduction(|: bad)
+#endif
+    for (int64_t j = 0; j < M; ++j) {
+        for (int32_t l = 0; l < d; ++l) Cb[j * d + l] = (float)orc_bf16(C[j * d + l]);
+        /* O2: norm of the bf16 cache row */
+        double q = 0.0;
+        for (int32_t l = 0; l < d; ++l) q += (double)Cb[j * d + l] * (double)Cb[j * d + l];
+        nc[j] = sqrt(q);
+        if (!(nc[j] > 0.0) || !isfinite(nc[j])) bad = 1;
+    }
+    for (int64_t e = 0; e < (int64_t)N * d; ++e) Xb[e] = (float)orc_bf16(X[e]);
+    if (bad) { free(Cb); free(Xb); free(nc); return ORC_EINVAL; }
+    int badq = 0;
+#ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 1) reduction(|: badq)
 #endif
     for (int32_t i = 0; i < N; ++i) {
-        const float* x = X + (int64_t)i * d;
+        const float* x = Xb + (int64_t)i * d;
         double* bs = topk_score + (int64_t)i * k;
         uint32_t* bg = topk_idx + (int64_t)i * k;
-        double nx = norm_bf16(x, d);
+        double nx = 0.0;
+        for (int32_t l = 0; l < d; ++l) nx += (double)x[l] * (double)x[l];
+        nx = sqrt(nx);                                               /* O2 */
         for (int32_t t = 0; t < k; ++t) { bs[t] = -1.0; bg[t] = 0xFFFFFFFFu; }
         if (!(nx > 0.0) || !isfinite(nx)) { badq = 1; continue; }
         int filled = 0;
         for (int64_t j = 0; j < M; ++j) {
-            double s = dot_bf16(x, C + j * d, d) / (nx * nc[j]);   /* O3 */
+            const float* c = Cb + j * d;
+            double dot = 0.0;
+            for (int32_t l = 0; l < d; ++l) dot += (double)x[l] * (double)c[l];
+            double s = dot / (nx * nc[j]);                           /* O3 */
             uint32_t g = ids ? ids[j] : (uint32_t)j;
             /* O4: insert (s, g) into the sorted best-k list */
             if (filled < k || better(s, g, bs[k - 1], bg[k - 1])) {
@@ -136,7 +155,7 @@ int orc_scan_topk(const float* X, int32_t N, const float* C, int64_t M, int32_t 
             }
         }
     }
-    free(nc);
+    free(Cb); free(Xb); free(nc);
     return badq ? ORC_EINVAL : ORC_OK;
 }
 

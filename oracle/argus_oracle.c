@@ -166,7 +166,7 @@ int orc_scan_topk(const float* X, int32_t N, const float* C, int64_t M, int32_t 
 int orc_mlp(const float* X, const double* S, int32_t N, int32_t d, int32_t k, int32_t H, int32_t L,
             const float* W1, const float* b1, const float* W2, const float* b2, int nthreads,
             double* rhat) {
-    if (N < 0 || d <= 0 || k <= 0 || H <= 0 || L <= 0) return ORC_EINVAL;
+    if (N < 0 || d <= 0 || k < 0 || H <= 0 || L <= 0) return ORC_EINVAL;  /* k = 0: SM-mode classifier */
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(static)

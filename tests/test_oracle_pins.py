@@ -190,6 +190,23 @@ def test_mlp_closed_forms_and_numpy_forward():
     np.testing.assert_allclose(oracle.mlp(X, S, W1, b1, W2, b2), want, rtol=1e-12, atol=1e-13)
 
 
+def test_mlp_sm_mode_numpy_forward():
+    """k = 0 (SM mode: a classifier on the prompt alone): numpy fp64 forward."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(61)
+    N, d, H, L = 7, 64, 32, 6
+    X = rng.standard_normal((N, d)).astype(np.float32)
+    W1 = rng.standard_normal((H, d)).astype(np.float32)
+    b1 = rng.standard_normal(H).astype(np.float32)
+    W2 = rng.standard_normal((L, H)).astype(np.float32)
+    b2 = rng.standard_normal(L).astype(np.float32)
+    bf = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64).numpy()
+    h = np.maximum(bf(X) @ bf(W1).T + b1, 0)
+    want = 1 / (1 + np.exp(-(h @ W2.astype(np.float64).T + b2)))
+    want[:, 0] = 1.0
+    np.testing.assert_allclose(oracle.mlp(X, np.zeros((N, 0)), W1, b1, W2, b2), want, rtol=1e-12, atol=1e-13)
+
+
 # ------------------------------------------------------------------ O6..O8 compliance (S:67)
 def _opts(L, pth=None, gates=None, kskip=None):
     pth = list(range(10, 10 + L)) if pth is None else pth

@@ -88,8 +88,12 @@ typedef struct {
 } argus_option;
 
 /* Router configuration.
- *   d          embedding dimension, multiple of 64, 64 <= d <= 768 (CLIP d=768)
- *   k          top-k, 1 <= k <= 8
+ *   d          embedding dimension, multiple of 64, 64 <= d <= 1024 (CLIP d=768,
+ *              OpenCLIP-H d=1024)
+ *   k          top-k, 0 <= k <= 8.  k = 0 is the paper's SM mode (smaller model
+ *              variants, no cache retrieval): no scan, the predictor
+ *              sees the prompt embedding only (w1 is [hidden][d]), every option must
+ *              have k_skip = 0, topk outputs may be NULL
  *   L          number of options, 1 <= L <= 32
  *   hidden     predictor hidden width H, multiple of 32, 32 <= H <= 1024
  *   max_batch  largest N a route call may pass, 1 <= max_batch <= 8192
@@ -99,6 +103,9 @@ typedef struct {
  *   nccl_unique_id        128-byte ncclUniqueId identical on all ranks, or NULL
  *                         (world == 1, or external collective mode)
  *   stream     cudaStream_t to run on, or NULL (the library creates one)
+ *   evict      0: an insert past capacity fails (ARGUS_E_CAPACITY).  1: ring
+ *              eviction of the oldest entries (capacity % world == 0); see
+ *              argus_cache_insert_h
  *   pipeline   0: every call's work is ordered on `stream`.  1 (single GPU,
  *              argus_route_batch_dev only): the fused tail of batch b (merge,
  *              predictor, A5, assignment) runs on an internal high-priority
@@ -115,6 +122,7 @@ typedef struct {
   const void* nccl_unique_id;
   void* stream;
   int32_t pipeline;
+  int32_t evict;
 } argus_config;
 
 /* Create an ncclUniqueId (128 bytes) on rank 0; share it with the other ranks
@@ -199,6 +207,120 @@ int argus_sync(argus_router* r);
  * fractional parts t_v - c_v, ties to the lower v.  sum c = N.
  * f [L] >= 0 finite with S > 0, 1 <= L <= 64, N >= 0; c_out [L]. */
 int argus_quota_from_fractions(const double* f, int32_t L, int32_t N, int32_t* c_out);
+
+/* ------------------------------------------------ control plane
+ *
+ * The paper's per-minute loop ("Every minute, we solve ..."): the allocator
+ * solves Eq. 1 for the load shares F(v) (argus_solve_allocation); the workload
+ * distribution predictor's affinity histogram H(v) of optimal options over the
+ * last 1000 prompts (argus_affinity_histogram) and F feed ODA
+ * (argus_oda_pasm), whose PASM the prompt scheduler samples per prompt
+ * (argus_set_policy with ARGUS_POLICY_PASM).  Eq. 3 then picks a
+ * worker for every prompt (argus_set_workers).  Quotas for the default
+ * serial-dictatorship policy come from F via argus_quota_from_fractions. */
+
+/* Eq. 1 for n_workers homogeneous workers and L levels (slow -> fast):
+ * maximise sum_v Q_v F(v), F(v) = Y_v / W, subject to each worker running at most
+ * one level and carrying an integer load y_w <= floor(p_th[v_w]) (QPM) with
+ * sum_w y_w = W.  Exact (dynamic program over compositions, loads water-filled in
+ * decreasing Q).  W = 0: every worker on level 0, loads 0, F = e_0.  W above the
+ * cluster's capacity: every worker on the fastest level at capacity and
+ * *feasible_out = 0 ("saturated plan flagged infeasible").
+ *   Q [L] profiled relative quality, p_th [L] peak throughput (QPM)
+ *   level_out [n_workers] level of worker w (or NULL), load_out [n_workers] y_w (or
+ *   NULL), F_out [L] load shares (or NULL), objective_out sum_v Q_v Y_v / served
+ *   (or NULL), feasible_out (or NULL).  Host only; no router needed.
+ * Errors: ARGUS_E_INVALID (ranges, non-finite, (L+1)(n_workers+1)(W+1) > 2^24). */
+int argus_solve_allocation(int32_t W, int32_t n_workers, int32_t L, const double* Q, const float* p_th,
+                           int32_t* level_out, int32_t* load_out, double* F_out, double* objective_out,
+                           int32_t* feasible_out);
+
+/* Algorithm 1, the Optimized Distribution Aligner.  H [L] affinity
+ * histogram (counts or shares, >= 0, sum > 0), F [L] target load shares (>= 0,
+ * sum > 0), both normalised to distributions; levels slow (0) -> fast (L-1).
+ * pasm_out [L][L] row-major: pasm_out[i*L + j] = P(v'_j | v_i), the probability
+ * that a prompt whose optimal level is v_i is served at v'_j; rows of levels with
+ * H = 0 are the identity.  Per-origin mass bookkeeping realises the paper's chain
+ * composition of step probabilities (R19).  Host only. */
+int argus_oda_pasm(const double* H, const double* F, int32_t L, double* pasm_out);
+
+/* Eq. 2: *dq_out = sum_i sum_{j : p_th[j] > p_th[i]} pasm[i][j] H[i] D[j][i],
+ * D [L][L] row-major (D[j*L + i] = degradation of serving a v_i-optimal prompt at v'_j). */
+int argus_pasm_degradation(const double* pasm, const double* H, const float* p_th, const double* D, int32_t L,
+                           double* dq_out);
+
+#define ARGUS_POLICY_SD 0    /* quota-capped serial dictatorship (row A6, the default)   */
+#define ARGUS_POLICY_PASM 1  /* sample the PASM row of each prompt's optimal option     */
+#define ARGUS_AFFINITY_WINDOW 1000
+
+/* Select the assignment policy of the router (collective when world > 1; every
+ * rank must pass the same arguments).  ARGUS_POLICY_PASM: pasm [L][L] as from
+ * argus_oda_pasm (rows >= 0, each with positive sum; rows are used as given);
+ * for prompt i of the b-th routing call after this one (b = 0, 1, ...):
+ *   o_i = the optimal option: among C_i the largest p_th, then the larger r,
+ *         then the lower index (DESIGN R18);
+ *   u_i = (x >> 8) * 2^-24 with x the first word of Philox4x32-10(counter =
+ *         {i, b mod 2^32, b >> 32, 0}, key = {seed mod 2^32, seed >> 32});
+ *   a_i = the first j with u_i < cdf[o_i][j], cdf the float32 running sums of the
+ *         row (float32 adds, j ascending); if none, the last j with pasm > 0;
+ *   an inadmissible a_i (similarity gate) falls back to the largest admissible
+ *         option below it (DESIGN R21).
+ * Quotas are ignored (may be NULL) under PASM; status gets NONCOMPLIANT when
+ * r_{i,a_i} < delta and GATED_ALL as usual; OVERFLOW never.
+ * ARGUS_POLICY_SD: pasm and seed ignored.  Errors: ARGUS_E_INVALID. */
+int argus_set_policy(argus_router* r, int32_t policy, const double* pasm, uint64_t seed);
+
+/* Affinity histogram H(v): counts of the optimal options o_i of the last
+ * min(routed, ARGUS_AFFINITY_WINDOW) prompts routed by this router (both
+ * policies).  counts_out [L]; *n_out = number of prompts counted.  Synchronises
+ * the router. */
+int argus_affinity_histogram(argus_router* r, int64_t* counts_out, int64_t* n_out);
+
+/* Worker selector (Eq. 3).  n_workers in [0, 1024] (0 disables);
+ * option_of_worker [n] = the option v worker w serves (-1 = none; at most 32
+ * workers per option), t_proc [n] its per-image time (> 0, finite), queue [n] its
+ * current queue length R_queue,w (>= 0).  Each routed batch then assigns, for
+ * prompts in index order, w_i = argmin over the workers serving a_i of
+ * fl32(float(R_w) * t_w), ties to the lower w, and increments R_{w_i}; prompts
+ * whose option no worker serves get -1.  The queues live in device memory; a later
+ * argus_set_workers call replaces them (e.g. after completions). */
+int argus_set_workers(argus_router* r, int32_t n_workers, const int32_t* option_of_worker, const float* t_proc,
+                      const int32_t* queue);
+
+/* Current queue lengths R_queue,w [n_workers] (synchronises the router). */
+int argus_get_queues(argus_router* r, int32_t* queue_out);
+
+/* Optional outputs of argus_route_batch_ex / argus_route_batch_ex_dev (any member
+ * may be NULL; host buffers for the host call, device buffers for the _dev call):
+ *   optimal      [N] int32   o_i, the prompt's optimal option ("optimal model
+ *                            choice"), as defined under argus_set_policy
+ *   worker       [N] int32   the Eq. 3 worker of the assigned option, -1 if no worker
+ *                            serves it (requires argus_set_workers)
+ *   topk_handle  [N][k] u64  the latent handle stored with each returned cache entry
+ *                            (argus_cache_insert_h; 0 for none / padding), i.e. the
+ *                            intermediate-state reference the worker fetches */
+typedef struct {
+  int32_t* optimal;
+  int32_t* worker;
+  uint64_t* topk_handle;
+} argus_route_extra;
+
+/* argus_route_batch / argus_route_batch_dev plus the outputs in *extra (NULL = none). */
+int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                         int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
+                         uint8_t* status_out, const argus_route_extra* extra);
+int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t N, const int32_t* quota,
+                             int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
+                             float* quality_dev, uint8_t* status_dev, const argus_route_extra* extra);
+
+/* Cache lifecycle ("Each prompt stores intermediate states at K"): append n
+ * entries like argus_cache_insert and store handles [n] (u64, caller-defined, e.g.
+ * an object-store key of the 144 KB intermediate state; NULL = 0) with them.
+ * With cfg.evict = 1 a full cache overwrites its oldest entries (ring): the live
+ * entries are always the last min(M, capacity) inserted, ids keep counting
+ * (global id g lives at cache position g mod capacity), and a rejected insert
+ * (non-finite / zero-norm row) leaves the cache unchanged. */
+int argus_cache_insert_h(argus_router* r, const float* emb, const uint64_t* handles, int64_t n, int64_t* first_id);
 
 /* Number of cache entries inserted so far (global, identical on all ranks). */
 int argus_cache_size(const argus_router* r, int64_t* m_out);

@@ -32,7 +32,9 @@ SYMBOLS = (
     "argus_route_batch", "argus_route_batch_dev", "argus_route_partial_dev", "argus_route_finish_dev",
     "argus_route_join", "argus_sync", "argus_quota_from_fractions", "argus_cache_size", "argus_launch_count",
     "argus_get_stream", "argus_profile_enable", "argus_profile_read", "argus_route_destroy",
-    "argus_strerror",
+    "argus_strerror", "argus_solve_allocation", "argus_oda_pasm", "argus_pasm_degradation", "argus_set_policy",
+    "argus_affinity_histogram", "argus_set_workers", "argus_get_queues", "argus_route_batch_ex",
+    "argus_route_batch_ex_dev", "argus_cache_insert_h",
 )
 STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
@@ -46,7 +48,12 @@ class argus_config(C.Structure):
     _fields_ = [("d", C.c_int32), ("k", C.c_int32), ("L", C.c_int32), ("hidden", C.c_int32),
                 ("max_batch", C.c_int32), ("capacity", C.c_int64), ("delta", C.c_float),
                 ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pipeline", C.c_int32)]
+                ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p), ("pipeline", C.c_int32),
+                ("evict", C.c_int32)]
+
+
+class argus_route_extra(C.Structure):
+    _fields_ = [("optimal", C.c_void_p), ("worker", C.c_void_p), ("topk_handle", C.c_void_p)]
 
 
 class ArgusError(RuntimeError):
@@ -80,6 +87,16 @@ def _load():
         "argus_profile_read": [P, C.c_int, P, P],
         "argus_route_destroy": [P],
         "argus_strerror": [C.c_int],
+        "argus_solve_allocation": [I32, I32, I32, P, P, P, P, P, P, P],
+        "argus_oda_pasm": [P, P, I32, P],
+        "argus_pasm_degradation": [P, P, P, P, I32, P],
+        "argus_set_policy": [P, I32, P, C.c_uint64],
+        "argus_affinity_histogram": [P, P, P],
+        "argus_set_workers": [P, I32, P, P, P],
+        "argus_get_queues": [P, P],
+        "argus_route_batch_ex": [P, P, I32, P, P, P, P, P, P, P],
+        "argus_route_batch_ex_dev": [P, P, I32, P, P, P, P, P, P, P],
+        "argus_cache_insert_h": [P, P, P, I64, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -129,11 +146,50 @@ def argus_strerror(code: int) -> str:
     return strerror(code)
 
 
+POLICY_SD, POLICY_PASM = 0, 1
+AFFINITY_WINDOW = 1000
+
+
+def argus_solve_allocation(W: int, n_workers: int, Q, p_th):
+    """Eq. 1 allocator (host).  Returns dict(levels, loads, F, objective, feasible)."""
+    Q = np.ascontiguousarray(Q, np.float64)
+    p_th = np.ascontiguousarray(p_th, np.float32)
+    L = Q.size
+    lv = np.empty(n_workers, np.int32)
+    ld = np.empty(n_workers, np.int32)
+    F = np.empty(L, np.float64)
+    obj, feas = C.c_double(), C.c_int32()
+    _check(_lib.argus_solve_allocation(int(W), int(n_workers), L, _p(Q), _p(p_th), _p(lv), _p(ld), _p(F),
+                                       C.byref(obj), C.byref(feas)), "argus_solve_allocation")
+    return dict(levels=lv, loads=ld, F=F, objective=obj.value, feasible=bool(feas.value))
+
+
+def argus_oda_pasm(H, F) -> np.ndarray:
+    """Algorithm 1 (host): PASM [L][L], row = optimal level, column = served level."""
+    H = np.ascontiguousarray(H, np.float64)
+    F = np.ascontiguousarray(F, np.float64)
+    P = np.empty((H.size, H.size), np.float64)
+    _check(_lib.argus_oda_pasm(_p(H), _p(F), H.size, _p(P)), "argus_oda_pasm")
+    return P
+
+
+def argus_pasm_degradation(pasm, H, p_th, D) -> float:
+    pasm = np.ascontiguousarray(pasm, np.float64)
+    H = np.ascontiguousarray(H, np.float64)
+    p_th = np.ascontiguousarray(p_th, np.float32)
+    D = np.ascontiguousarray(D, np.float64)
+    dq = C.c_double()
+    _check(_lib.argus_pasm_degradation(_p(pasm), _p(H), _p(p_th), _p(D), H.size, C.byref(dq)),
+           "argus_pasm_degradation")
+    return dq.value
+
+
 class Router:
     """Owner of one ``argus_router*``.  Methods map 1:1 onto the C ABI."""
 
     def __init__(self, d, k, opts, W1, b1, W2, b2, capacity, max_batch, hidden=None,
-                 delta=0.9, rank=0, world=1, device=0, nccl_unique_id=None, stream=None, pipeline=False):
+                 delta=0.9, rank=0, world=1, device=0, nccl_unique_id=None, stream=None, pipeline=False,
+                 evict=False):
         L = len(opts)
         self.d, self.k, self.L = int(d), int(k), L
         W1 = np.ascontiguousarray(W1, np.float32)
@@ -150,7 +206,7 @@ class Router:
         cfg = argus_config(self.d, self.k, L, H, self.max_batch, int(capacity), float(delta),
                            int(rank), int(world), int(device),
                            C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
-                           C.c_void_p(stream) if stream else None, int(bool(pipeline)))
+                           C.c_void_p(stream) if stream else None, int(bool(pipeline)), int(bool(evict)))
         self._keep = [np.ascontiguousarray(x, np.float32) for x in (W1, b1, W2, b2)]
         h = C.c_void_p()
         _check(_lib.argus_route_init(C.byref(cfg), oa, *[_p(x) for x in self._keep], C.byref(h)),
@@ -228,6 +284,63 @@ class Router:
         return _check(_lib.argus_route_batch_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
                                                  _p(topk_idx), _p(topk_score), _p(quality), _p(status)),
                       "argus_route_batch_dev")
+
+    def argus_route_batch_ex(self, prompts, quota, want_workers=False, want_handles=False):
+        """Host-buffer route with the optimal options (and Eq. 3 workers, latent
+        handles).  quota may be None under the PASM policy.  Returns (rc, outputs)."""
+        prompts = np.ascontiguousarray(prompts, np.float32)
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
+        N = prompts.shape[0]
+        out = dict(option=np.empty(N, np.int32), topk_idx=np.empty((N, self.k), np.uint32),
+                   topk_score=np.empty((N, self.k), np.float32), quality=np.empty((N, self.L), np.float32),
+                   status=np.empty(N, np.uint8), optimal=np.empty(N, np.int32),
+                   worker=np.empty(N, np.int32) if want_workers else None,
+                   topk_handle=np.empty((N, self.k), np.uint64) if want_handles else None)
+        ex = argus_route_extra(_p(out["optimal"]), _p(out["worker"]), _p(out["topk_handle"]))
+        rc = _check(_lib.argus_route_batch_ex(self._h, _p(prompts), N, _p(quota), _p(out["option"]),
+                                              _p(out["topk_idx"]), _p(out["topk_score"]), _p(out["quality"]),
+                                              _p(out["status"]), C.byref(ex)), "argus_route_batch_ex")
+        return rc, out
+
+    def argus_route_batch_ex_dev(self, prompts_dev, quota, option, topk_idx, topk_score, quality=None,
+                                 status=None, optimal=None, worker=None, topk_handle=None, N=None):
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
+        N = int(prompts_dev.shape[0]) if N is None else int(N)
+        ex = argus_route_extra(_p(optimal), _p(worker), _p(topk_handle))
+        return _check(_lib.argus_route_batch_ex_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
+                                                    _p(topk_idx), _p(topk_score), _p(quality), _p(status),
+                                                    C.byref(ex)), "argus_route_batch_ex_dev")
+
+    def argus_cache_insert_h(self, emb, handles=None) -> int:
+        emb = np.ascontiguousarray(emb, np.float32).reshape(-1, self.d)
+        h = None if handles is None else np.ascontiguousarray(handles, np.uint64)
+        first = C.c_int64(-1)
+        _check(_lib.argus_cache_insert_h(self._h, _p(emb), _p(h), emb.shape[0], C.byref(first)),
+               "argus_cache_insert_h")
+        return first.value
+
+    def argus_set_policy(self, policy, pasm=None, seed=0):
+        pasm = None if pasm is None else np.ascontiguousarray(pasm, np.float64)
+        _check(_lib.argus_set_policy(self._h, int(policy), _p(pasm), C.c_uint64(int(seed))), "argus_set_policy")
+
+    def argus_affinity_histogram(self):
+        """(counts [L] int64, prompts counted)."""
+        h = np.empty(self.L, np.int64)
+        n = C.c_int64()
+        _check(_lib.argus_affinity_histogram(self._h, _p(h), C.byref(n)), "argus_affinity_histogram")
+        return h, n.value
+
+    def argus_set_workers(self, option_of_worker, t_proc, queue):
+        ow = np.ascontiguousarray(option_of_worker, np.int32)
+        t = np.ascontiguousarray(t_proc, np.float32)
+        q = np.ascontiguousarray(queue, np.int32)
+        self._n_workers = int(ow.size)
+        _check(_lib.argus_set_workers(self._h, ow.size, _p(ow), _p(t), _p(q)), "argus_set_workers")
+
+    def argus_get_queues(self) -> np.ndarray:
+        q = np.empty(getattr(self, "_n_workers", 0), np.int32)
+        _check(_lib.argus_get_queues(self._h, _p(q)), "argus_get_queues")
+        return q
 
     def argus_route_partial_dev(self, prompts_dev, keys_dev, N=None):
         N = int(prompts_dev.shape[0]) if N is None else int(N)

@@ -137,6 +137,22 @@ struct argus_router {
   uint8_t* h_outblk = nullptr;     // pinned mirror
   size_t outblk_bytes = 0;
   bool pending = false;            // async (_dev) work enqueued since the last argus_sync
+  // F1 (policy, PASM, affinity window) and F3 (Eq. 3 workers)
+  int32_t policy = 0;              // ARGUS_POLICY_SD / ARGUS_POLICY_PASM
+  uint64_t seed = 0;
+  uint64_t batch_seq = 0;          // routing calls since argus_set_policy (Philox counter)
+  float* d_cdf = nullptr;          // [32][32] float32 running sums of the PASM rows
+  int8_t* d_plast = nullptr;       // [32]
+  uint8_t* d_aff = nullptr;        // [ARGUS_AFFINITY_WINDOW] ring of optimal options
+  int64_t aff_total = 0;           // prompts routed (ring position)
+  int32_t n_workers = 0;
+  int16_t* d_wlist = nullptr;      // [32][32]
+  int32_t* d_wcount = nullptr;     // [32]
+  float* d_wtime = nullptr;        // [MAX_WORKERS]
+  int32_t* d_queue = nullptr;      // [MAX_WORKERS]
+  uint64_t* d_handle = nullptr;    // [capacity] latent handles by cache position (replicated on every rank)
+  int32_t* d_optimal = nullptr;    // [max_batch] host-path staging of o_i
+  int32_t* d_worker = nullptr;     // [max_batch] host-path staging of worker ids
   CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   // stage profiling (argus_profile_*)
@@ -146,6 +162,8 @@ struct argus_router {
   double prof_ms[ARGUS_NUM_STAGES] = {};
   int64_t prof_n[ARGUS_NUM_STAGES] = {};
 };
+
+constexpr int MAX_WORKERS = 1024;
 
 // ------------------------------------------------------------------ helpers
 #define CU_TRY(r, expr)                                               \
@@ -372,7 +390,9 @@ int argus_route_destroy(argus_router* r) {
                   r->d_mlp_cnt, r->d_tail_cnt, r->d_Cb, r->d_invc, r->d_Xstage, r->d_Xb[0], r->d_Xb[1],
                   r->d_invq[0], r->d_invq[1], r->d_partial[0], r->d_partial[1], r->d_keys, r->d_keys_all,
                   r->d_score, r->d_idx, r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option,
-                  r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1]};
+                  r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1], r->d_cdf, r->d_plast,
+                  r->d_aff, r->d_wlist, r->d_wcount, r->d_wtime, r->d_queue, r->d_optimal, r->d_worker,
+                  r->d_handle};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -397,7 +417,9 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   *out = nullptr;
   const argus_config& c = *cfg;
   if (c.d < 64 || c.d % 64 != 0 || !scan_supported(c.d)) return ARGUS_E_INVALID;
-  if (c.k < 1 || c.k > 8) return ARGUS_E_INVALID;
+  if (c.k < 0 || c.k > 8) return ARGUS_E_INVALID;  // k = 0: SM mode (no cache)
+  if (c.evict != 0 && c.evict != 1) return ARGUS_E_INVALID;
+  if (c.evict && (c.capacity < c.world || c.capacity % c.world != 0)) return ARGUS_E_INVALID;
   if (c.L < 1 || c.L > 32) return ARGUS_E_INVALID;
   if (c.hidden < 32 || c.hidden > 1024 || c.hidden % 32 != 0) return ARGUS_E_INVALID;
   if (tail_smem_bytes(c.d, c.k, c.hidden, c.L, c.max_batch, 148) > 220 * 1024) return ARGUS_E_INVALID;
@@ -410,6 +432,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     if (!opts || !w1 || !b1 || !w2 || !b2) return ARGUS_E_INVALID;
     if (opts[0].k_skip != 0) return ARGUS_E_INVALID;
     for (int v = 0; v < c.L; ++v) {
+      if (c.k == 0 && opts[v].k_skip != 0) return ARGUS_E_INVALID;  // SM mode: model variants only
       if (opts[v].k_skip < 0 || opts[v].k_skip >= 50) return ARGUS_E_INVALID;
       if (!std::isfinite(opts[v].p_th_qpm)) return ARGUS_E_INVALID;
       if (v > 0 && opts[v].p_th_qpm < opts[v - 1].p_th_qpm) return ARGUS_E_INVALID;
@@ -505,7 +528,17 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_status, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_option, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_order, (size_t)c.max_batch));
-  r->outblk_bytes = 16 + 16 * 5 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1);
+  TRY_RC(dalloc(r, &r->d_cdf, 32 * 32));
+  TRY_RC(dalloc(r, &r->d_plast, 32));
+  TRY_RC(dalloc(r, &r->d_aff, ARGUS_AFFINITY_WINDOW));
+  TRY_RC(dalloc(r, &r->d_wlist, 32 * 32));
+  TRY_RC(dalloc(r, &r->d_wcount, 32));
+  TRY_RC(dalloc(r, &r->d_wtime, MAX_WORKERS));
+  TRY_RC(dalloc(r, &r->d_queue, MAX_WORKERS));
+  TRY_RC(dalloc(r, &r->d_optimal, (size_t)c.max_batch));
+  TRY_RC(dalloc(r, &r->d_handle, (size_t)std::max<int64_t>(c.capacity, 1)));
+  TRY_RC(dalloc(r, &r->d_worker, (size_t)c.max_batch));
+  r->outblk_bytes = 16 + 16 * 8 + (size_t)c.max_batch * (4 + 16 * (size_t)k + 4 * (size_t)L + 1 + 8);
   TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
   r->d_flags = reinterpret_cast<uint32_t*>(r->d_outblk);
   if (cudaMallocHost((void**)&r->h_outblk, r->outblk_bytes) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
@@ -521,7 +554,9 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
       cudaMemsetAsync(r->d_invc, 0, (size_t)(r->cap_local + 256) * sizeof(float), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_flags, 0, sizeof(uint32_t), r->stream) != cudaSuccess ||
       cudaMemsetAsync(r->d_mlp_cnt, 0, sizeof(int32_t) * (size_t)(n16 / 16), r->stream) != cudaSuccess ||
-      cudaMemsetAsync(r->d_tail_cnt, 0, sizeof(int32_t), r->stream) != cudaSuccess) {
+      cudaMemsetAsync(r->d_tail_cnt, 0, sizeof(int32_t), r->stream) != cudaSuccess ||
+      cudaMemsetAsync(r->d_handle, 0, sizeof(uint64_t) * (size_t)std::max<int64_t>(c.capacity, 1), r->stream) !=
+          cudaSuccess) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
@@ -603,7 +638,8 @@ int argus_get_stream(const argus_router* r, void** stream_out) {
   return ARGUS_OK;
 }
 
-static int insert_impl(argus_router* r, const float* emb, int64_t n, int64_t* first_id, bool on_device) {
+static int insert_impl(argus_router* r, const float* emb, int64_t n, int64_t* first_id, bool on_device,
+                       const uint64_t* handles = nullptr) {
   int rc = check_state(r);
   if (rc) return rc;
   if (n < 0) return ARGUS_E_INVALID;
@@ -611,48 +647,85 @@ static int insert_impl(argus_router* r, const float* emb, int64_t n, int64_t* fi
   if (rc) return rc;
   const bool root = r->cfg.rank == 0 || !nccl_mode(r);
   if (root && n > 0 && !emb) return ARGUS_E_INVALID;
-  if (r->m_global + n > r->cfg.capacity) return ARGUS_E_CAPACITY;
+  const int64_t cap = r->cfg.capacity;
+  if (!r->cfg.evict && r->m_global + n > cap) return ARGUS_E_CAPACITY;
+  if (r->cfg.evict && r->m_global + n > (int64_t)0xFFFFFFFE) return ARGUS_E_CAPACITY;  // 32-bit global ids
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d;
-  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
-  for (int64_t off = 0; off < n; off += INSERT_CHUNK) {
-    const int64_t m = std::min<int64_t>(INSERT_CHUNK, n - off);
-    const float* src = nullptr;
-    if (root) {
-      if (on_device && !nccl_mode(r)) {
-        src = emb + off * d;
+  // with eviction an insert overwrites live rows, so validate everything first (dry
+  // pass, no writes); without it rows past M are simply not yet counted
+  const int passes = r->cfg.evict ? 2 : 1;
+  // with eviction only the last `cap` rows of this call survive
+  const int64_t skip = (r->cfg.evict && n > cap) ? n - cap : 0;
+  uint32_t fl = 0;
+  for (int pass = 0; pass < passes; ++pass) {
+    const bool dry = passes == 2 && pass == 0;
+    CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+    for (int64_t off = dry ? 0 : skip; off < n; off += INSERT_CHUNK) {
+      const int64_t m = std::min<int64_t>(INSERT_CHUNK, n - off);
+      const float* src = nullptr;
+      if (root) {
+        if (on_device && !nccl_mode(r)) {
+          src = emb + off * d;
+        } else {
+          CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, emb + off * d, sizeof(float) * m * d,
+                                    on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, r->stream));
+          src = r->d_Xstage;
+        }
       } else {
-        CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, emb + off * d, sizeof(float) * m * d,
-                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, r->stream));
         src = r->d_Xstage;
       }
-    } else {
-      src = r->d_Xstage;
+      if (nccl_mode(r))  // C-3: rank 0's rows to every rank; each keeps its stripe
+        NC_TRY(r, nccl().Broadcast(r->d_Xstage, r->d_Xstage, (size_t)m * d, ncclFloat32, 0, r->comm, r->stream));
+      {
+        StageScope sc(r, ARGUS_STAGE_INSERT);
+        launch_insert_rows(src, m, r->m_global + off, d, r->cfg.rank, r->cfg.world, cap, dry, r->d_Cb, r->d_invc,
+                           r->d_flags, r->stream);
+      }
+      LAUNCHED(r);
     }
-    if (nccl_mode(r))  // C-3: rank 0's rows to every rank; each keeps its stripe
-      NC_TRY(r, nccl().Broadcast(r->d_Xstage, r->d_Xstage, (size_t)m * d, ncclFloat32, 0, r->comm, r->stream));
-    {
-      StageScope sc(r, ARGUS_STAGE_INSERT);
-      launch_insert_rows(src, m, r->m_global + off, d, r->cfg.rank, r->cfg.world, r->d_Cb, r->d_invc,
-                         r->d_flags, r->stream);
-    }
-    LAUNCHED(r);
-  }
-  CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
-  CU_TRY(r, cudaStreamSynchronize(r->stream));
-  uint32_t fl = *r->h_flags;
-  if (nccl_mode(r)) {  // every rank must agree on validity (each saw only its stripe)
-    CU_TRY(r, cudaMemcpyAsync(r->d_flags, &fl, 4, cudaMemcpyHostToDevice, r->stream));
-    NC_TRY(r, nccl().AllReduce(r->d_flags, r->d_flags, 1, ncclUint32, ncclMax, r->comm, r->stream));
     CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
     CU_TRY(r, cudaStreamSynchronize(r->stream));
     fl = *r->h_flags;
+    if (nccl_mode(r)) {  // every rank must agree on validity (each saw only its stripe)
+      CU_TRY(r, cudaMemcpyAsync(r->d_flags, &fl, 4, cudaMemcpyHostToDevice, r->stream));
+      NC_TRY(r, nccl().AllReduce(r->d_flags, r->d_flags, 1, ncclUint32, ncclMax, r->comm, r->stream));
+      CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
+      CU_TRY(r, cudaStreamSynchronize(r->stream));
+      fl = *r->h_flags;
+    }
+    CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
+    if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;  // cache unchanged (M not advanced / dry pass)
   }
-  CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
-  if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;  // M unchanged: rows past M are ignored
+  // latent handles ("intermediate noise (144 KB) stored in ... EFS"): one u64 per
+  // entry at its cache position, replicated on every rank; absent handles read 0
+  if (n > skip) {
+    std::vector<uint64_t> hs((size_t)(n - skip), 0);
+    if (root && handles) memcpy(hs.data(), handles + skip, sizeof(uint64_t) * hs.size());
+    uint64_t* dst_stage = reinterpret_cast<uint64_t*>(r->d_Xstage);
+    for (int64_t off = 0; off < (int64_t)hs.size();) {
+      const int64_t g = r->m_global + skip + off;
+      const int64_t pos = g % std::max<int64_t>(cap, 1);
+      const int64_t run = std::min<int64_t>({(int64_t)hs.size() - off, cap - pos, (int64_t)INSERT_CHUNK});
+      if (nccl_mode(r)) {
+        CU_TRY(r, cudaMemcpyAsync(dst_stage, hs.data() + off, sizeof(uint64_t) * run, cudaMemcpyHostToDevice,
+                                  r->stream));
+        NC_TRY(r, nccl().Broadcast(dst_stage, r->d_handle + pos, (size_t)run, ncclUint64, 0, r->comm, r->stream));
+      } else {
+        CU_TRY(r, cudaMemcpyAsync(r->d_handle + pos, hs.data() + off, sizeof(uint64_t) * run,
+                                  cudaMemcpyHostToDevice, r->stream));
+      }
+      off += run;
+    }
+    CU_TRY(r, cudaStreamSynchronize(r->stream));  // hs is a host temporary
+  }
   if (first_id) *first_id = r->m_global;
   r->m_global += n;
   return ARGUS_OK;
+}
+
+int argus_cache_insert_h(argus_router* r, const float* emb, const uint64_t* handles, int64_t n, int64_t* first_id) {
+  return insert_impl(r, emb, n, first_id, false, handles);
 }
 
 int argus_cache_insert(argus_router* r, const float* emb, int64_t n, int64_t* first_id) {
@@ -663,9 +736,16 @@ int argus_cache_insert_dev(argus_router* r, const float* emb_dev, int64_t n, int
   return insert_impl(r, emb_dev, n, first_id, true);
 }
 
+static int64_t live_rows(const argus_router* r) {  // global entries currently held
+  return std::min<int64_t>(r->m_global, r->cfg.capacity);
+}
 static int64_t local_rows(const argus_router* r) {
   const int64_t G = r->cfg.world, rk = r->cfg.rank;
-  return (r->m_global + G - 1 - rk) / G;
+  return (live_rows(r) + G - 1 - rk) / G;
+}
+// ring eviction: cache position of the oldest live entry (age index 0)
+static int64_t ring_head(const argus_router* r) {
+  return (r->cfg.evict && r->m_global > r->cfg.capacity) ? r->m_global % r->cfg.capacity : 0;
 }
 
 // K6 + scan (+ K5 local merge into keys_dev when keys_dev != NULL).  *P_out receives
@@ -720,7 +800,13 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     NC_TRY(r, nccl().Broadcast(r->d_invq[q], r->d_invq[q], (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
     NC_TRY(r, nccl().GroupEnd());
   }
+  if (k == 0) {  // SM mode: no cache scan, the tail sees the prompts only
+    *P_out = 0;
+    return ARGUS_OK;
+  }
   ScanArgs a{};
+  a.head = (uint32_t)ring_head(r);
+  a.capg = r->cfg.evict ? (uint32_t)r->cfg.capacity : 0u;
   a.Xb = r->d_Xb[q];
   a.inv_q = r->d_invq[q];
   a.Cb = r->d_Cb;
@@ -756,7 +842,14 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 // The fused tail (merge of P candidate lists per prompt, predictor, A5, assignment).
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, cudaStream_t s, bool pdl);
+                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr);
+static int quota_ok(const argus_router* r, const int32_t* quota) {
+  if (r->policy == ARGUS_POLICY_PASM) return 1;  // quotas are not used when sampling the PASM
+  if (!quota) return 0;
+  for (int v = 0; v < r->cfg.L; ++v)
+    if (quota[v] < 0) return 0;
+  return 1;
+}
 
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
@@ -768,13 +861,13 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
 
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, cudaStream_t s, bool pdl) {
+                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex) {
   int rc = check_state(r);
   if (rc) return rc;
-  if (N < 1 || N > r->cfg.max_batch || P < 1 || !keys_in || !quota) return ARGUS_E_INVALID;
+  const bool sm_mode = r->cfg.k == 0;
+  if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota)) return ARGUS_E_INVALID;
+  if (!sm_mode && (P < 1 || !keys_in)) return ARGUS_E_INVALID;
   const int L = r->cfg.L, k = r->cfg.k;
-  for (int v = 0; v < L; ++v)
-    if (quota[v] < 0) return ARGUS_E_INVALID;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   TailArgs m{};
   m.keys_in = keys_in;
@@ -805,28 +898,58 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
-  for (int v = 0; v < 32; ++v) m.quota[v] = v < L ? quota[v] : 0;
+  for (int v = 0; v < 32; ++v) m.quota[v] = (v < L && quota) ? quota[v] : 0;
   m.option_out = option_out_dev ? option_out_dev : r->d_option;
   m.status = status_dev ? status_dev : r->d_status;
   m.flags = r->d_flags;
+  m.policy = r->policy;
+  m.pasm_cdf = r->d_cdf;
+  m.pasm_last = r->d_plast;
+  m.seed_lo = (uint32_t)r->seed;
+  m.seed_hi = (uint32_t)(r->seed >> 32);
+  m.seq_lo = (uint32_t)r->batch_seq;
+  m.seq_hi = (uint32_t)(r->batch_seq >> 32);
+  m.optimal_out = ex ? ex->optimal : nullptr;
+  m.id_base = (uint32_t)(r->m_global - live_rows(r));
+  m.head = (uint32_t)ring_head(r);
+  m.capg = r->cfg.evict ? (uint32_t)r->cfg.capacity : 0u;
+  m.handle = r->d_handle;
+  m.topk_handle = ex ? ex->topk_handle : nullptr;
+  m.aff_ring = r->d_aff;
+  m.aff_win = ARGUS_AFFINITY_WINDOW;
+  m.aff_pos0 = (int32_t)(r->aff_total % ARGUS_AFFINITY_WINDOW);
+  m.n_workers = r->n_workers;
+  m.wlist = r->d_wlist;
+  m.wcount = r->d_wcount;
+  m.wtime = r->d_wtime;
+  m.queue = r->d_queue;
+  m.worker_out = ex ? ex->worker : nullptr;
   {
     StageScope sc(r, ARGUS_STAGE_TAIL, s);
     launch_tail(m, r->tail_smem, s, pdl);
   }
   LAUNCHED(r);
+  r->batch_seq++;
+  r->aff_total += N;
   return ARGUS_OK;
 }
 
 int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, const int32_t* quota,
                           int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
                           float* quality_dev, uint8_t* status_dev) {
+  return argus_route_batch_ex_dev(r, prompts_dev, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
+                                  quality_dev, status_dev, nullptr);
+}
+
+int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t N, const int32_t* quota,
+                             int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
+                             float* quality_dev, uint8_t* status_dev, const argus_route_extra* ex) {
   int rc = check_state(r);
   if (rc) return rc;
   if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;  // external mode: use partial/finish
-  if (N < 1 || N > r->cfg.max_batch || !quota || !option_out_dev || !topk_idx_dev || !topk_score_dev)
+  if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota) || !option_out_dev ||
+      (r->cfg.k > 0 && (!topk_idx_dev || !topk_score_dev)))
     return ARGUS_E_INVALID;
-  for (int v = 0; v < r->cfg.L; ++v)
-    if (quota[v] < 0) return ARGUS_E_INVALID;
   r->pending = true;
   int32_t P = 0;
   if (r->pipe) {  // prep / scan / tail on the internal streams (see the file header)
@@ -839,7 +962,7 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->scan_stream));
     CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_scan[q], 0));
     rc = finish_impl(r, r->d_partial[q], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                     status_dev, r->tail_stream, false);
+                     status_dev, r->tail_stream, false, ex);
     if (rc) return rc;
     CU_TRY(r, cudaEventRecord(r->ev_tail[q], r->tail_stream));
     r->tail_inflight[q] = true;
@@ -850,14 +973,15 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N, 
     rc = partial_impl(r, prompts_dev, N, nullptr, &P, 0);
     if (rc) return rc;
     return finish_impl(r, r->d_partial[0], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
-                       status_dev, r->stream, true);
+                       status_dev, r->stream, true, ex);
   }
   rc = partial_impl(r, prompts_dev, N, r->d_keys, &P, 0);
   if (rc) return rc;
   // C-2: N*k candidate keys from every shard
-  NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
+  if (r->cfg.k > 0)
+    NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
   return finish_impl(r, r->d_keys_all, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
-                     quality_dev, status_dev, r->stream, true);
+                     quality_dev, status_dev, r->stream, true, ex);
 }
 
 int argus_route_join(argus_router* r, void* stream) {
@@ -898,10 +1022,22 @@ int argus_sync(argus_router* r) {
 int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
                       int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
                       uint8_t* status_out) {
+  return argus_route_batch_ex(r, prompts, N, quota, option_out, topk_idx, topk_score, quality_out, status_out,
+                              nullptr);
+}
+
+int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                         int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
+                         uint8_t* status_out, const argus_route_extra* extra) {
   int rc = check_state(r);
   if (rc) return rc;
   const bool root = r->cfg.rank == 0 || !nccl_mode(r);
-  if (N < 1 || N > r->cfg.max_batch || !quota || !option_out || !topk_idx || !topk_score) return ARGUS_E_INVALID;
+  if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota) || !option_out ||
+      (r->cfg.k > 0 && (!topk_idx || !topk_score)))
+    return ARGUS_E_INVALID;
+  int32_t* optimal_out = extra ? extra->optimal : nullptr;
+  int32_t* worker_out = extra ? extra->worker : nullptr;
+  uint64_t* handle_out = extra ? extra->topk_handle : nullptr;
   if (root && !prompts) return ARGUS_E_INVALID;
   if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
@@ -910,35 +1046,146 @@ int argus_route_batch(argus_router* r, const float* prompts, int32_t N, const in
     rc = argus_sync(r);
     if (rc < 0) return rc;
   }
-  for (int v = 0; v < L; ++v)
-    if (quota[v] < 0) return ARGUS_E_INVALID;
-  // packed output block for this N: [flags | option | idx | score | rhat | status]
+  // packed output block for this N: [flags | option | idx | score | rhat | status | optimal | worker | handle]
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t o_opt = 16, o_idx = al(o_opt + 4 * (size_t)N), o_sc = al(o_idx + 4 * (size_t)N * k),
-               o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L), o_end = o_st + N;
+               o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L), o_ob = al(o_st + N),
+               o_wk = al(o_ob + 4 * (size_t)N), o_hd = al(o_wk + 4 * (size_t)N), o_end = o_hd + 8 * (size_t)N * k;
+  const size_t o_copy = handle_out ? o_end : worker_out ? o_hd : (optimal_out ? o_wk : o_ob);
   uint8_t* D = r->d_outblk;
   if (root)
     CU_TRY(r, cudaMemcpyAsync(r->d_Xstage, prompts, sizeof(float) * N * d, cudaMemcpyHostToDevice, r->stream));
-  rc = argus_route_batch_dev(r, r->d_Xstage, N, quota, reinterpret_cast<int32_t*>(D + o_opt),
-                             reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
-                             reinterpret_cast<float*>(D + o_rh), D + o_st);
+  argus_route_extra dx{optimal_out ? reinterpret_cast<int32_t*>(D + o_ob) : nullptr,
+                       worker_out ? reinterpret_cast<int32_t*>(D + o_wk) : nullptr,
+                       handle_out ? reinterpret_cast<uint64_t*>(D + o_hd) : nullptr};
+  rc = argus_route_batch_ex_dev(r, r->d_Xstage, N, quota, reinterpret_cast<int32_t*>(D + o_opt),
+                                reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
+                                reinterpret_cast<float*>(D + o_rh), D + o_st, &dx);
   if (rc) return rc;
   rc = argus_route_join(r, nullptr);
   if (rc) return rc;
-  CU_TRY(r, cudaMemcpyAsync(r->h_outblk, D, o_end, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaMemcpyAsync(r->h_outblk, D, o_copy, cudaMemcpyDeviceToHost, r->stream));
   CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
   CU_TRY(r, cudaStreamSynchronize(r->stream));
   r->pending = false;
-  const uint8_t* H = r->h_outblk;
-  memcpy(option_out, H + o_opt, 4 * (size_t)N);
-  memcpy(topk_idx, H + o_idx, 4 * (size_t)N * k);
-  memcpy(topk_score, H + o_sc, 4 * (size_t)N * k);
-  if (quality_out) memcpy(quality_out, H + o_rh, 4 * (size_t)N * L);
-  if (status_out) memcpy(status_out, H + o_st, (size_t)N);
+  const uint8_t* Hb = r->h_outblk;
+  memcpy(option_out, Hb + o_opt, 4 * (size_t)N);
+  if (k > 0) {
+    memcpy(topk_idx, Hb + o_idx, 4 * (size_t)N * k);
+    memcpy(topk_score, Hb + o_sc, 4 * (size_t)N * k);
+  }
+  if (handle_out) memcpy(handle_out, Hb + o_hd, 8 * (size_t)N * k);
+  if (quality_out) memcpy(quality_out, Hb + o_rh, 4 * (size_t)N * L);
+  if (status_out) memcpy(status_out, Hb + o_st, (size_t)N);
+  if (optimal_out) memcpy(optimal_out, Hb + o_ob, 4 * (size_t)N);
+  if (worker_out) memcpy(worker_out, Hb + o_wk, 4 * (size_t)N);
   uint32_t fl;
-  memcpy(&fl, H, 4);
+  memcpy(&fl, Hb, 4);
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
+  return ARGUS_OK;
+}
+
+// ------------------------------------------------------------------ F1 / F3 router state
+int argus_set_policy(argus_router* r, int32_t policy, const double* pasm, uint64_t seed) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  const int L = r->cfg.L;
+  if (policy != ARGUS_POLICY_SD && policy != ARGUS_POLICY_PASM) return ARGUS_E_INVALID;
+  float cdf[32 * 32] = {};
+  int8_t last[32] = {};
+  if (policy == ARGUS_POLICY_PASM) {
+    if (!pasm) return ARGUS_E_INVALID;
+    for (int o = 0; o < L; ++o) {
+      double srow = 0.0;
+      float c = 0.0f;
+      int lj = -1;
+      for (int j = 0; j < L; ++j) {
+        const double p = pasm[o * L + j];
+        if (!std::isfinite(p) || p < 0.0) return ARGUS_E_INVALID;
+        srow += p;
+        const float pf = (float)p;
+        c = c + pf;  // float32 running sum, j ascending (the decision precision, DESIGN R20)
+        cdf[o * 32 + j] = c;
+        if (pf > 0.0f) lj = j;
+      }
+      if (!(srow > 0.0) || lj < 0) return ARGUS_E_INVALID;
+      last[o] = (int8_t)lj;
+    }
+  }
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = argus_route_join(r, nullptr);  // batches in flight keep the policy they were issued with
+  if (rc) return rc;
+  CU_TRY(r, cudaMemcpyAsync(r->d_cdf, cdf, sizeof(cdf), cudaMemcpyHostToDevice, r->stream));
+  CU_TRY(r, cudaMemcpyAsync(r->d_plast, last, sizeof(last), cudaMemcpyHostToDevice, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));  // the host tables are stack arrays
+  r->policy = policy;
+  r->seed = seed;
+  r->batch_seq = 0;
+  return ARGUS_OK;
+}
+
+int argus_affinity_histogram(argus_router* r, int64_t* counts_out, int64_t* n_out) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (!counts_out) return ARGUS_E_INVALID;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = argus_route_join(r, nullptr);
+  if (rc) return rc;
+  uint8_t ring[ARGUS_AFFINITY_WINDOW];
+  CU_TRY(r, cudaMemcpyAsync(ring, r->d_aff, sizeof(ring), cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));
+  const int64_t n = std::min<int64_t>(r->aff_total, ARGUS_AFFINITY_WINDOW);
+  for (int v = 0; v < r->cfg.L; ++v) counts_out[v] = 0;
+  // the last n prompts occupy ring slots (aff_total - n .. aff_total - 1) mod W
+  for (int64_t t = r->aff_total - n; t < r->aff_total; ++t) {
+    const int o = ring[t % ARGUS_AFFINITY_WINDOW];
+    if (o < r->cfg.L) counts_out[o]++;
+  }
+  if (n_out) *n_out = n;
+  return ARGUS_OK;
+}
+
+int argus_set_workers(argus_router* r, int32_t n_workers, const int32_t* option_of_worker, const float* t_proc,
+                      const int32_t* queue) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  const int L = r->cfg.L;
+  if (n_workers < 0 || n_workers > MAX_WORKERS) return ARGUS_E_INVALID;
+  if (n_workers > 0 && (!option_of_worker || !t_proc || !queue)) return ARGUS_E_INVALID;
+  std::vector<int16_t> wl(32 * 32, -1);
+  std::vector<int32_t> wc(32, 0);
+  for (int w = 0; w < n_workers; ++w) {
+    const int v = option_of_worker[w];
+    if (v < -1 || v >= L || !std::isfinite(t_proc[w]) || !(t_proc[w] > 0.f) || queue[w] < 0) return ARGUS_E_INVALID;
+    if (v < 0) continue;
+    if (wc[v] == 32) return ARGUS_E_INVALID;
+    wl[v * 32 + wc[v]++] = (int16_t)w;
+  }
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = argus_route_join(r, nullptr);
+  if (rc) return rc;
+  if (n_workers > 0) {
+    CU_TRY(r, cudaMemcpyAsync(r->d_wlist, wl.data(), sizeof(int16_t) * wl.size(), cudaMemcpyHostToDevice, r->stream));
+    CU_TRY(r, cudaMemcpyAsync(r->d_wcount, wc.data(), sizeof(int32_t) * wc.size(), cudaMemcpyHostToDevice, r->stream));
+    CU_TRY(r, cudaMemcpyAsync(r->d_wtime, t_proc, sizeof(float) * n_workers, cudaMemcpyHostToDevice, r->stream));
+    CU_TRY(r, cudaMemcpyAsync(r->d_queue, queue, sizeof(int32_t) * n_workers, cudaMemcpyHostToDevice, r->stream));
+  }
+  CU_TRY(r, cudaStreamSynchronize(r->stream));  // host arrays may be freed after return
+  r->n_workers = n_workers;
+  return ARGUS_OK;
+}
+
+int argus_get_queues(argus_router* r, int32_t* queue_out) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (!queue_out) return ARGUS_E_INVALID;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = argus_route_join(r, nullptr);
+  if (rc) return rc;
+  if (r->n_workers > 0)
+    CU_TRY(r, cudaMemcpyAsync(queue_out, r->d_queue, sizeof(int32_t) * r->n_workers, cudaMemcpyDeviceToHost, r->stream));
+  CU_TRY(r, cudaStreamSynchronize(r->stream));
   return ARGUS_OK;
 }
 

@@ -23,7 +23,7 @@ __device__ __forceinline__ float row_to_bf16(const float* __restrict__ src, __nv
     b |= !isfinite(r.x) || !isfinite(r.y);
     acc = __fmaf_rn(r.x, r.x, acc);
     acc = __fmaf_rn(r.y, r.y, acc);
-    dst[j] = h;
+    if (dst) dst[j] = h;
   }
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, m));
@@ -33,18 +33,21 @@ __device__ __forceinline__ float row_to_bf16(const float* __restrict__ src, __nv
 }
 
 __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t g0, int d,
-                              int rank, int world, __nv_bfloat16* __restrict__ Cb,
+                              int rank, int world, int64_t cap, int dry, __nv_bfloat16* __restrict__ Cb,
                               float* __restrict__ inv_c, uint32_t* flags) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n; i += nw) {
     const int64_t g = g0 + i;
-    if (g % world != rank) continue;
-    const int64_t slot = g / world;
+    // cache position g mod capacity (ring eviction; g < capacity otherwise), striped:
+    // rank pos % world holds it at slot pos / world (capacity % world == 0 when evicting)
+    const int64_t pos = cap > 0 ? g % cap : g;
+    if (!dry && pos % world != rank) continue;
+    const int64_t slot = pos / world;
     bool bad;
-    float ss = row_to_bf16(rows + i * d, reinterpret_cast<__nv_bfloat162*>(Cb + slot * d), d, &bad);
+    float ss = row_to_bf16(rows + i * d, dry ? nullptr : reinterpret_cast<__nv_bfloat162*>(Cb + slot * d), d, &bad);
     if ((threadIdx.x & 31) == 0) {
-      inv_c[slot] = bad ? 0.f : __fdiv_rn(1.0f, __fsqrt_rn(ss));
+      if (!dry) inv_c[slot] = bad ? 0.f : __fdiv_rn(1.0f, __fsqrt_rn(ss));
       if (bad) atomicOr(flags, FLAG_INVALID_INPUT);
     }
   }
@@ -75,15 +78,15 @@ __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, in
   pdl_launch();
 }
 
-void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank,
-                        int32_t world, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags,
-                        cudaStream_t s) {
+void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank, int32_t world,
+                        int64_t cap, bool dry, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags, cudaStream_t s) {
   if (n <= 0) return;
   const int threads = 256;
   int64_t warps = n;
   int64_t blocks = (warps * 32 + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_insert_rows<<<(unsigned)blocks, threads, 0, s>>>(rows, n, g0, d, rank, world, Cb, inv_c, flags);
+  k_insert_rows<<<(unsigned)blocks, threads, 0, s>>>(rows, n, g0, d, rank, world, cap, dry ? 1 : 0, Cb, inv_c,
+                                                     flags);
 }
 
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,

@@ -24,6 +24,7 @@
 //     threshold shared (monotonically) with the other lists of the same prompt.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 3 = idle,
 // 4..11 = Q loader + epilogue.
+#include <cstddef>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -40,37 +41,58 @@ namespace {
 constexpr int TN = 64;                      // cache rows per tile (UMMA N)
 constexpr int TM = 128;                     // prompts per CTA (UMMA M)
 constexpr int KBLK = 64;                    // bf16 per 128-byte swizzle row
-constexpr int KB_MAX = 12;                  // d <= 768
+constexpr int KB_TMEM = 12;                 // k-blocks of the prompt slice resident in TMEM (d <= 768)
+constexpr int KB_MAX = 16;                  // d <= 1024: k-blocks 12..15 of A stay in shared memory
 constexpr int BOX_BYTES = TN * KBLK * 2;    // 8 KB cache box
-constexpr int HALF_BOXES = KB_MAX / 2;      // a tile streams through two half-tile slots
-constexpr int SLOT_BYTES = HALF_BOXES * BOX_BYTES;  // 48 KB
-constexpr int NSLOT = 4;                    // ring of half-tile slots (2 tiles)
-constexpr int RING_BYTES = NSLOT * SLOT_BYTES;      // 192 KB (also holds the 128 x d prompt slice at start)
+constexpr int QBOX_BYTES = TM * KBLK * 2;   // 16 KB prompt box
+constexpr int NSLOT = 4;                    // ring of tile-part slots
+constexpr int REGION_BYTES = 192 * 1024;    // ring (+ A tail); also holds 12 prompt boxes at start
 constexpr int THREADS = 384;               // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
-constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (d <= 768)
+constexpr int ACC_COL0 = 384;               // accumulators after the resident Q (12 k-blocks)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int INV_SLOTS = 8;
 constexpr int CHUNK = 4;                    // tiles per dynamically scheduled work unit
 constexpr size_t SCRATCH_OFF = 4096;        // after the barriers: 8 warps x 16 x 32 fp32 slow-path scratch
-constexpr size_t SMEM_BYTES = (size_t)RING_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
+constexpr size_t SMEM_BYTES = (size_t)REGION_BYTES + 1024 /*align*/ + SCRATCH_OFF + EPI_WARPS * 16 * 32 * 4;
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+
+// Shape of one variant.  KBV = 12 (d <= 768): a tile streams through SPT = 2
+// half-tile slots of 6 boxes (48 KB), the whole prompt slice is in TMEM.  KBV = 16
+// (768 < d <= 1024): k-blocks 12..15 of the prompt slice (the "A tail", 64 KB) stay
+// in shared memory at the start of the region and are read by the MMA through a
+// descriptor; a tile streams through SPT = 4 quarter-tile slots of 4 boxes (32 KB)
+// behind it.  Either way TMEM = 384 columns of A + 2 x 64 accumulator columns.
+template <int KBV>
+struct Shape {
+  static constexpr int SPT = KBV == 12 ? 2 : 4;                 // slots per tile
+  static constexpr int SLOT_BOXES = KBV / SPT;                  // 6 or 4
+  static constexpr int SLOT_BYTES = SLOT_BOXES * BOX_BYTES;     // 48 or 32 KB
+  static constexpr int ATAIL_BYTES = (KBV - KB_TMEM) * QBOX_BYTES;  // 0 or 64 KB
+  static constexpr int RING0 = ATAIL_BYTES;                     // ring offset in the region
+  static_assert(RING0 + NSLOT * SLOT_BYTES <= REGION_BYTES, "region");
+  static_assert(KB_TMEM * QBOX_BYTES <= REGION_BYTES, "prompt staging");
+};
 }  // namespace
 
-struct ScanSmem {  // placed after the ring
-  uint64_t full[NSLOT];         // TMA boxes of half-tile slot s landed
-  uint64_t empty[NSLOT];        // MMAs reading slot s complete (one commit per half tile); for a
-                                // tile's second half this also means the accumulator is final
+struct ScanSmem {  // placed after the region
+  uint64_t full[NSLOT];         // TMA boxes of slot s landed
+  uint64_t empty[NSLOT];        // MMAs reading slot s complete (one commit per slot); with SPT = 2
+                                // the tile's last slot completing also means the accumulator is final
   uint64_t tempty[2];           // epilogue has read accumulator b
-  uint64_t qfull;               // prompt slice landed in shared memory
+  uint64_t afull[2];            // SPT = 4: accumulator b final (extra commit after the tile's last slot)
+  uint64_t qfull;               // prompt slice (TMEM part) landed in shared memory
   uint64_t qready;              // prompt slice is in TMEM; buffers may be reused
+  uint64_t atail;               // KBV = 16: A tail landed in shared memory
   uint64_t invfull[INV_SLOTS];  // inv_c slot l % 8 landed (cannot lap, see the epilogue); also
                                 // publishes tile_id[l % 8] (-1 = no more tiles)
   int64_t tile_id[INV_SLOTS];   // cache tile of the CTA's l-th tile
   uint32_t tmem_base;
   uint32_t pad_[3];
-  float invc[INV_SLOTS][TN];    // inverse cache-row norms of tile l in slot l % 8 (bulk copy)
+  alignas(16) float invc[INV_SLOTS][TN];  // inverse cache-row norms of tile l in slot l % 8 (bulk copy)
 };
+static_assert(offsetof(ScanSmem, invc) % 16 == 0, "bulk-copy / float4 destination");
+static_assert(sizeof(ScanSmem) <= SCRATCH_OFF, "barriers fit before the scratch");
 
 // Epilogue on 32 accumulator columns (cache rows c0 .. c0+31 of the tile) of one
 // prompt.  Fast path (2 instructions per score): x_c = acc_c * inv_c[c] and a
@@ -81,7 +103,8 @@ struct ScanSmem {  // placed after the ring
 // exact score s = fl(x * inv_q) and inserts into its register top-k.
 template <int KMAX>
 __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float iq, int cmax, uint32_t g0,
-                                          uint32_t world, TopList<KMAX>& tl, float& thr, uint32_t scratch) {
+                                          uint32_t world, uint32_t head, uint32_t capg, TopList<KMAX>& tl,
+                                          float& thr, uint32_t scratch) {
   const int lane = threadIdx.x & 31;
   float m = -INFINITY;
 #pragma unroll
@@ -119,7 +142,10 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
             mask &= mask - 1;
             const float sc = __fmul_rn(tc::lds_f32(scratch + (uint32_t)(c * 32 + lane) * 4), iq);
             if (sc >= thr) {
-              tl.insert(pack_key(sc, g0 + (uint32_t)(half * 16 + c) * world));
+              // key id = age of the entry (0 = oldest live): the cache position itself
+              // unless a ring-evicting cache has wrapped (head > 0)
+              const uint32_t pos = g0 + (uint32_t)(half * 16 + c) * world;
+              tl.insert(pack_key(sc, pos >= head ? pos - head : pos + capg - head));
               if (tl.v[KMAX - 1] != 0) thr = fmaxf(thr, key_score(tl.v[KMAX - 1]));
             }
           }
@@ -130,14 +156,17 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
   }
 }
 
-template <int KMAX>
+template <int KMAX, int KBV>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
               int slices, int64_t n_tiles, int l2mode) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)RING_BYTES);
-  const uint32_t ring_s = tc::smem_u32(ring);
+  using SH = Shape<KBV>;
+  constexpr int SPT = SH::SPT;
+  ScanSmem* sm = reinterpret_cast<ScanSmem*>(ring + (size_t)REGION_BYTES);
+  const uint32_t region_s = tc::smem_u32(ring);           // prompt staging, then [A tail | ring]
+  const uint32_t ring_s = region_s + (uint32_t)SH::RING0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x % slices;
   const int range = blockIdx.x / slices;  // index of this CTA's candidate list
@@ -151,7 +180,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_init(tc::smem_u32(&sm->empty[s]), 1);
     }
     for (int b = 0; b < 2; ++b) tc::mbar_init(tc::smem_u32(&sm->tempty[b]), 32 * EPI_WARPS);
+    for (int b = 0; b < 2; ++b) tc::mbar_init(tc::smem_u32(&sm->afull[b]), 1);
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
+    tc::mbar_init(tc::smem_u32(&sm->atail), 1);
     for (int s = 0; s < INV_SLOTS; ++s) tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
     tc::mbar_init(tc::smem_u32(&sm->qready), 32 * EPI_WARPS);
     tc::fence_barrier_init();
@@ -169,18 +200,25 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producer
     if (lane == 0) {
-      // prompt slice: KB boxes of 128 rows x 64 bf16 (16 KB, 128-byte swizzle) into the buffers
+      // prompt slice: its first min(KB, 12) boxes of 128 rows x 64 bf16 (16 KB, 128-byte
+      // swizzle) into the region, to be moved into TMEM by the epilogue warps
+      const int KBT = KB < KB_TMEM ? KB : KB_TMEM;
       const uint32_t qb = tc::smem_u32(&sm->qfull);
-      tc::mbar_arrive_expect_tx(qb, (uint32_t)(KB * TM * KBLK * 2));
-      for (int kb = 0; kb < KB; ++kb)
-        tc::tma_load_2d(ring_s + (uint32_t)(kb * TM * KBLK * 2), &tmap_q, qb, kb * KBLK, slice * TM);
-      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // ring free again
+      tc::mbar_arrive_expect_tx(qb, (uint32_t)(KBT * QBOX_BYTES));
+      for (int kb = 0; kb < KBT; ++kb)
+        tc::tma_load_2d(region_s + (uint32_t)(kb * QBOX_BYTES), &tmap_q, qb, kb * KBLK, slice * TM);
+      tc::mbar_wait(tc::smem_u32(&sm->qready), 0);  // region free again
+      if (KBV > KB_TMEM) {  // the A tail (k-blocks 12..KB-1) stays in shared memory for the whole kernel
+        const uint32_t ab = tc::smem_u32(&sm->atail);
+        tc::mbar_arrive_expect_tx(ab, (uint32_t)((KB - KB_TMEM) * QBOX_BYTES));
+        for (int kb = KB_TMEM; kb < KB; ++kb)
+          tc::tma_load_2d(region_s + (uint32_t)((kb - KB_TMEM) * QBOX_BYTES), &tmap_q, ab, kb * KBLK, slice * TM);
+      }
       // one slice streams the cache exactly once: evict-first; with several slices the
       // other slices re-read each tile from L2 shortly after the first reader
       const int l2m = l2mode & 15;
       const uint64_t pol = l2m == 0 ? tc::policy_evict_first()
                                     : (l2m == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
-      const int kb_half[2] = {(KB + 1) / 2, KB / 2};
       int* ctr = a.ctr + slice;
       int64_t l = 0;
       // static split (diagnostics): CTA `range` takes chunks [c_lo, c_hi) in order
@@ -193,21 +231,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         c = l2mode >= 16 ? c + 1 : atomicAdd(ctr, 1);  // next chunk: the latency overlaps this chunk's loads
         const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
         for (int64_t t = t0; t < t1; ++t, ++l) {
-          for (int hh = 0; hh < 2; ++hh) {
-            const int64_t u = 2 * l + hh;  // half-tile sequence number
+#pragma unroll
+          for (int hh = 0; hh < SPT; ++hh) {
+            const int64_t u = SPT * l + hh;  // slot sequence number
             const int sl = (int)(u & (NSLOT - 1));
             tc::mbar_wait(tc::smem_u32(&sm->empty[sl]), (uint32_t)(((u >> 2) & 1) ^ 1));
             const uint32_t fb = tc::smem_u32(&sm->full[sl]);
-            tc::mbar_arrive_expect_tx(fb, (uint32_t)(kb_half[hh] * BOX_BYTES));
+            const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
+            tc::mbar_arrive_expect_tx(fb, (uint32_t)((kb1 - kb0) * BOX_BYTES));
             if (hh == 0) {  // the tile's id and inverse norms (rows past capacity read zeros)
               sm->tile_id[l & (INV_SLOTS - 1)] = t;
               const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
               tc::mbar_arrive_expect_tx(ib, TN * 4);
               tc::bulk_load_hint(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib, pol);
             }
-            const int kb0 = hh ? kb_half[0] : 0;
-            for (int j = 0; j < kb_half[hh]; ++j)
-              tc::tma_load_2d_hint(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb,
+            for (int j = 0; j < kb1 - kb0; ++j)
+              tc::tma_load_2d_hint(ring_s + (uint32_t)(sl * SH::SLOT_BYTES + j * BOX_BYTES), &tmap_c, fb,
                                    (kb0 + j) * KBLK, (int32_t)(t * TN), pol);
           }
         }
@@ -215,7 +254,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       // end markers in the next two tile slots (one per MMA issuer; same reuse rule as
       // a real tile)
       for (int e = 0; e < 2; ++e, ++l) {
-        tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l) & (NSLOT - 1)]), (uint32_t)((((2 * l) >> 2) & 1) ^ 1));
+        const int64_t u = SPT * l;
+        tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 2) & 1) ^ 1));
         sm->tile_id[l & (INV_SLOTS - 1)] = -1;
         tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
       }
@@ -229,9 +269,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // of the committing thread only, so the two barrier sets stay independent.
     constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
     tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
+    if (KBV > KB_TMEM) tc::mbar_wait(tc::smem_u32(&sm->atail), 0);
     tc::fence_after();
-    const int kb_half0 = (KB + 1) / 2;
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
+    const uint64_t abase = tc::desc_kmajor_sw128(region_s);  // A tail (KBV = 16)
     const int lstep = (l2mode & 32) ? 1 : 2;
     for (int64_t l = warp == 1 ? 0 : 1;; l += lstep) {
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
@@ -241,25 +282,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::fence_after();
       const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int64_t u = 2 * l + hh;
+      for (int hh = 0; hh < SPT; ++hh) {
+        const int64_t u = SPT * l + hh;
         const int sl = (int)(u & (NSLOT - 1));
         tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 2) & 1));
         tc::fence_after();
-        const int kb0 = hh ? kb_half0 : 0;
-        const int nkb = hh ? KB - kb_half0 : kb_half0;
-        const uint64_t dslot = dbase + (uint64_t)((sl * SLOT_BYTES) >> 4);
-        for (int j = 0; j < nkb; ++j) {
+        const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
+        const uint64_t dslot = dbase + (uint64_t)((sl * SH::SLOT_BYTES) >> 4);
+        for (int j = 0; j < kb1 - kb0; ++j) {
           const int kb = kb0 + j;
+          if (KBV == KB_TMEM || kb < KB_TMEM) {
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk)
-            if (ARGUS_SCAN_EXP != 2 || (kb | kk) == 0)
-              tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
-                              dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
+            for (int kk = 0; kk < KBLK / 16; ++kk)
+              if (ARGUS_SCAN_EXP != 2 || (kb | kk) == 0)
+                tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
+                                dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
+          } else {  // A tail from shared memory (same SW128 K-major layout as the TMA box)
+#pragma unroll
+            for (int kk = 0; kk < KBLK / 16; ++kk)
+              tc::mma_ss_warp(d_tmem, abase + (uint64_t)(((kb - KB_TMEM) * QBOX_BYTES + kk * 32) >> 4),
+                              dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, 1u);
+          }
         }
-        // frees slot sl; after the second half it also marks accumulator b final
+        // frees slot sl; with SPT = 2 the tile's last slot also marks accumulator b final
         tc::mma_commit_warp(tc::smem_u32(&sm->empty[sl]));
       }
+      if (SPT != 2) tc::mma_commit_warp(tc::smem_u32(&sm->afull[b]));
     }
   } else if (warp >= 4) {
     // ======================= Q into TMEM (A operand), then the epilogue
@@ -271,8 +319,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     {
       tc::mbar_wait(tc::smem_u32(&sm->qfull), 0);
       const int sw = p_local & 7;  // 128-byte swizzle: 16-byte chunk j of row r sits at chunk j ^ (r % 8)
-      for (int c = h; c < KB; c += 2) {   // 64 bf16 = 32 TMEM columns per box; halves split the boxes
-        const uint32_t row = ring_s + (uint32_t)(c * TM * KBLK * 2 + p_local * 128);
+      const int KBT = KB < KB_TMEM ? KB : KB_TMEM;
+      for (int c = h; c < KBT; c += 2) {   // 64 bf16 = 32 TMEM columns per box; halves split the boxes
+        const uint32_t row = region_s + (uint32_t)(c * QBOX_BYTES + p_local * 128);
         uint32_t r[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -291,7 +340,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    const uint32_t scratch = ring_s + (uint32_t)(RING_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
+    const uint32_t scratch = region_s + (uint32_t)(REGION_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;  // padded prompts never take the slow path
@@ -311,9 +360,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (gk != 0) thr = fmaxf(thr, key_score(gk));
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
-      // the tile's second half-slot (2l+1) % 4 completing means all its MMAs are done;
-      // it cannot lap: reuse by tile l+2 needs this warp's release of tile l
-      tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l + 1) & (NSLOT - 1)]), (uint32_t)((l >> 1) & 1));
+      // SPT = 2: the tile's second half-slot (2l+1) % 4 completing means all its MMAs are
+      // done; it cannot lap: reuse by tile l+2 needs this warp's release of tile l.
+      // SPT = 4: every tile uses all four slots, so a dedicated per-accumulator barrier
+      // (completes once per 2 tiles, same no-lap argument).
+      if (SPT == 2)
+        tc::mbar_wait(tc::smem_u32(&sm->empty[(2 * l + 1) & (NSLOT - 1)]), (uint32_t)((l >> 1) & 1));
+      else
+        tc::mbar_wait(tc::smem_u32(&sm->afull[b]), (uint32_t)((l >> 1) & 1));
       tc::fence_after();
       uint32_t v[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + h * 32, v);
@@ -328,7 +382,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t icp = tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
-        epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, tl, thr, scratch);
+        epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, a.head, a.capg, tl,
+                        thr, scratch);
         // publish only a local bound that beats everything seen so far (rare after warm-up)
         if (active && tl.v[KMAX - 1] > published && tl.v[KMAX - 1] > gk) {
           published = tl.v[KMAX - 1];
@@ -340,7 +395,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // fold the two column halves of each prompt inside the CTA: half 1 parks its list
     // in the (now idle) tile buffers, half 0 merges and writes one list per range
-    const uint32_t xchg = ring_s + (uint32_t)((q * 32 + lane) * KMAX * 8);
+    const uint32_t xchg = ring_s + (uint32_t)((q * 32 + lane) * KMAX * 8);  // ring idle (MMAs done)
     if (h == 1) {
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2) tc::sts_u64(xchg + t2 * 8, tl.v[t2]);
@@ -376,15 +431,20 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
+template <int KMAX, int KBV>
+static void launch_variant(bool pdl, dim3 grid, cudaStream_t s, const CUtensorMap& tc_, const CUtensorMap& tq,
+                           const ScanArgs& a, int slices, int64_t n_tiles, int l2mode) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scan_tc<KMAX, KBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attr = true;
+  }
+  launch_pdl_opt(pdl, k_scan_tc<KMAX, KBV>, grid, dim3(THREADS), SMEM_BYTES, s, tc_, tq, a, slices, n_tiles, l2mode);
+}
+
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s, bool pdl) {
   const int slices = (a.N + TM - 1) / TM;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_scan_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    cudaFuncSetAttribute(k_scan_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    attr = true;
-  }
   const dim3 grid(slices * a.P);
   // L2 policy of the cache stream: evict-first for one slice, normal LRU when
   // several slices re-read each tile (ARGUS_SCAN_L2=0/1/2 overrides, experiments)
@@ -395,10 +455,14 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
   }
   static int stat = (getenv("ARGUS_SCAN_STATIC") ? 16 : 0) | (getenv("ARGUS_SCAN_1MMA") ? 32 : 0);
   const int l2mode = (l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1)) | stat;
-  if (a.k <= 4)
-    launch_pdl_opt(pdl, k_scan_tc<4>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
-  else
-    launch_pdl_opt(pdl, k_scan_tc<8>, grid, dim3(THREADS), SMEM_BYTES, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+  const bool wide = a.d / KBLK > KB_TMEM;
+  if (a.k <= 4) {
+    if (wide) launch_variant<4, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else launch_variant<4, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+  } else {
+    if (wide) launch_variant<8, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else launch_variant<8, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+  }
 }
 
 }  // namespace argus

@@ -202,6 +202,63 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
   if (tid == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
 }
 
+// ------------------------------------------------------------------ F1: PASM sampling
+// Philox4x32-10 (Salmon et al., SC'11), first output word only is used.
+__device__ __forceinline__ uint32_t philox_x0(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                              uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c0;
+}
+
+// ------------------------------------------------------------------ F3: Eq. 3
+// One warp per option v: lanes hold the workers serving v (<= 32, ascending id) and
+// their queue lengths; the warp walks the batch in index order (ballots over 32
+// prompts), and each prompt assigned v takes argmin (fl(float(R_w) * t_w), w), which
+// then increments.  Options are independent, so warps run them concurrently.
+__device__ void select_workers(const TailArgs& a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v = warp; v < a.L; v += TW) {
+    const int nw = a.wcount[v];
+    const int w = lane < nw ? (int)a.wlist[v * 32 + lane] : 0x7fffffff;
+    int q = lane < nw ? a.queue[w] : 0;
+    const float t = lane < nw ? a.wtime[w] : 0.f;
+    for (int c0 = 0; c0 < a.N; c0 += 32) {
+      const int i = c0 + lane;
+      const int o = i < a.N ? __ldcg(a.option_out + i) : -1;
+      uint32_t m = __ballot_sync(0xffffffffu, o == v);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        float cost = lane < nw ? __fmul_rn((float)q, t) : INFINITY;
+        int who = w;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+          const float oc = __shfl_xor_sync(0xffffffffu, cost, s);
+          const int ow = __shfl_xor_sync(0xffffffffu, who, s);
+          if (oc < cost || (oc == cost && ow < who)) {
+            cost = oc;
+            who = ow;
+          }
+        }
+        if (lane < nw && w == who) ++q;
+        if (lane == 0 && a.worker_out) a.worker_out[c0 + b] = nw > 0 ? who : -1;
+      }
+    }
+    if (lane < nw) a.queue[w] = q;
+  }
+}
+
 // ------------------------------------------------------------------ the fused tail
 __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
@@ -282,8 +339,14 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       const uint64_t key = mk[pl][hl];
       ss[pl * k + hl] = key_score(key);
       if (cc == 0) {
-        a.topk_idx[(int64_t)i * k + hl] = key_id(key);
+        const uint32_t age = key_id(key);  // 0xFFFFFFFF for an empty slot (M < k)
+        a.topk_idx[(int64_t)i * k + hl] = key == 0 ? 0xFFFFFFFFu : a.id_base + age;
         a.topk_score[(int64_t)i * k + hl] = key_score(key);
+        if (a.topk_handle) {
+          uint32_t pos = a.head + age;
+          if (a.capg && pos >= a.capg) pos -= a.capg;
+          a.topk_handle[(int64_t)i * k + hl] = key == 0 ? 0ull : a.handle[pos];
+        }
       }
     } else if (pl >= nP && hl < k) {
       ss[pl * k + hl] = 0.f;
@@ -430,10 +493,43 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     } else if (lane < a.Lw) {
       a.rankof[(int64_t)i * a.Lw + lane] = 0xFF;
     }
+    // optimal option o_i: the compliant option with the largest p_th, then
+    // the larger r, then the lower index (DESIGN R18); option 0 is always compliant
+    float kp = cmp ? pth : -INFINITY, kr = cmp ? rr : -INFINITY;
+    int kv = lane;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const float op = __shfl_xor_sync(0xffffffffu, kp, s), orr = __shfl_xor_sync(0xffffffffu, kr, s);
+      const int ov = __shfl_xor_sync(0xffffffffu, kv, s);
+      if (op > kp || (op == kp && (orr > kr || (orr == kr && ov < kv)))) {
+        kp = op;
+        kr = orr;
+        kv = ov;
+      }
+    }
+    const int oi = kp == -INFINITY ? 0 : kv;
+    uint8_t st = (gmask != 0 && pmask == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
+    if (a.policy == 1) {
+      // PASM sample: u = Philox word >> 8 scaled by 2^-24 (exact), the
+      // first option whose float32 running sum exceeds u, then the gate fallback
+      const uint32_t x0 = philox_x0((uint32_t)i, a.seq_lo, a.seq_hi, 0u, a.seed_lo, a.seed_hi);
+      const float u = (float)(x0 >> 8) * 5.9604644775390625e-8f;
+      const bool hit = act && u < a.pasm_cdf[oi * 32 + lane];
+      const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+      const int as = hm ? __ffs(hm) - 1 : (int)a.pasm_last[oi];
+      const uint32_t below = amask & (as >= 31 ? 0xffffffffu : ((2u << as) - 1u));
+      const int af = 31 - __clz(below);  // bit 0 is always admissible
+      if (lane == 0) {
+        a.option_out[i] = af;
+        if (!((cmask >> af) & 1u)) st |= 2u;  // ARGUS_ST_NONCOMPLIANT
+      }
+    }
     if (lane == 0) {
       a.ccount[i] = (uint8_t)__popc(cmask);
       a.cmask[i] = cmask;
-      a.status[i] = (gmask != 0 && pmask == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
+      a.status[i] = st;
+      if (a.optimal_out) a.optimal_out[i] = oi;
+      if (a.aff_win > 0 && i >= a.N - a.aff_win) a.aff_ring[(a.aff_pos0 + i) % a.aff_win] = (uint8_t)oi;
     }
   }
 
@@ -447,7 +543,11 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   __threadfence();
   if (tid == 0) *a.launch_cnt = 0;
   if (ARGUS_TAIL_TIMING) T[5] = gtimer();
-  assign_all(a, smraw);
+  if (a.policy == 0) assign_all(a, smraw);
+  if (a.n_workers > 0) {
+    __syncthreads();  // option_out of this CTA's own phase 3 is visible to the block
+    select_workers(a);
+  }
   if (ARGUS_TAIL_TIMING) {
     T[6] = gtimer();
     if (tid == 0)

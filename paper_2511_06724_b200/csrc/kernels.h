@@ -45,14 +45,14 @@ struct ScanArgs {
   int32_t P;                 // number of cache ranges (filled by the planner)
   uint64_t* gthr;            // [n_pad] per-prompt shared top-k threshold key (zeroed by K6)
   int32_t* ctr;              // [MAX_SLICES] per-slice tile-chunk work counters (zeroed by K6)
+  uint32_t head, capg;       // ring eviction: oldest live cache position, capacity (0, 0 when not wrapped)
 };
 constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts
 
 // K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
 // g % world == rank go to slot g / world.
-void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank,
-                        int32_t world, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags,
-                        cudaStream_t s);
+void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank, int32_t world,
+                        int64_t cap, bool dry, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags, cudaStream_t s);
 
 // K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
@@ -75,8 +75,12 @@ struct TailArgs {
   // phase M: candidate lists -> final top-k
   const uint64_t* keys_in;   // [P][N][k] candidate keys (per-range partials, or all-gathered shards)
   int32_t P;
-  uint32_t* topk_idx;        // [N][k] out
+  uint32_t* topk_idx;        // [N][k] out: global id = id_base + age index of the key
   float* topk_score;         // [N][k] out
+  uint32_t id_base;          // global id of the oldest live entry
+  uint32_t head, capg;       // cache position of age 0, capacity (ring eviction; 0, 0 otherwise)
+  const uint64_t* handle;    // [capacity] latent handles by cache position
+  uint64_t* topk_handle;     // [N][k] out or nullptr
   // predictor
   const __nv_bfloat16* Xb;   // [n_pad][d]
   const void* W1xF;          // W1x bf16 in mma.sync B-fragment order (see k_prep_w1_frag)
@@ -102,6 +106,21 @@ struct TailArgs {
   int32_t* option_out;       // [N] out
   uint8_t* status;           // [N] out
   uint32_t* flags;
+  // F1: optimal options, PASM sampling, affinity window
+  int32_t policy;            // 0 serial dictatorship (A6), 1 PASM sampling
+  const float* pasm_cdf;     // [32][32] float32 running sums of the PASM rows (row = optimal option)
+  const int8_t* pasm_last;   // [32] last option with positive mass per row
+  uint32_t seed_lo, seed_hi, seq_lo, seq_hi;  // Philox key / batch counter
+  int32_t* optimal_out;      // [N] o_i or nullptr
+  uint8_t* aff_ring;         // [aff_win] optimal options of the last aff_win prompts
+  int32_t aff_win, aff_pos0; // window length (0: off), ring slot of prompt 0
+  // F3: Eq. 3 worker selection (n_workers = 0: off)
+  int32_t n_workers;
+  const int16_t* wlist;      // [32][32] workers serving option v (ascending), -1 padded
+  const int32_t* wcount;     // [32]
+  const float* wtime;        // [n_workers] t_proc
+  int32_t* queue;            // [n_workers] R_queue (device state, updated)
+  int32_t* worker_out;       // [N] or nullptr
 };
 // K3+K4 (+K5 on one GPU): merge, predictor, A5 and the assignment in one launch.
 // pdl = false when the tail's producer is on another stream (pipelined mode):

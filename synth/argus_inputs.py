@@ -169,10 +169,22 @@ class CacheGen:
         for ci in range(self.n_chunks()):
             yield ci * CHUNK, self.chunk(ci)
 
-    def all(self) -> np.ndarray:
+    def all(self, threads: int = 1) -> np.ndarray:
+        """All M rows.  threads > 1 generates chunks concurrently (each chunk has its
+        own seeded stream, so the result does not depend on `threads`)."""
         out = np.empty((self.M, self.d), np.float32)
-        for a, c in self.chunks():
-            out[a:a + c.shape[0]] = c
+
+        def fill(ci):
+            c = self.chunk(ci)
+            out[ci * CHUNK:ci * CHUNK + c.shape[0]] = c
+
+        if threads <= 1:
+            for ci in range(self.n_chunks()):
+                fill(ci)
+        else:
+            import concurrent.futures as cf
+            with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+                list(ex.map(fill, range(self.n_chunks())))
         return out
 
     def rows_at(self, ids) -> np.ndarray:

@@ -10,6 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; run via gpurun")
+    config.addinivalue_line("markers", "full: BASELINE.json full-size workload (sampled oracle checks)")
 
 
 def gpu_available():

@@ -29,7 +29,8 @@ def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
     Xs = X[list(rows)]
     M = cache.shape[0]
     kk = min(k + 1, max(M, 1))
-    osc, oix = oracle.scan_topk(Xs, cache, kk)
+    osc, oix = oracle.scan_topk(Xs, cache, kk, ids=ids)
+    row_of = (lambda g: g) if ids is None else {int(g): j for j, g in enumerate(ids)}.__getitem__
     exempt, max_err = 0, 0.0
     for r, i in enumerate(rows):
         gi = [int(x) for x in gpu_idx[i]]
@@ -43,7 +44,7 @@ def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
         o_s = osc[r]
         o_i = [int(x) for x in oix[r]]
         # scores of the GPU's ids, in the oracle
-        g_true = np.array([oracle.cosine(X[i], cache[g]) for g in gi[:nreal]])
+        g_true = np.array([oracle.cosine(X[i], cache[row_of(g)]) for g in gi[:nreal]])
         err = np.abs(g_true - np.array(gs[:nreal]))
         max_err = max(max_err, float(err.max()))
         assert err.max() <= SCORE_TOL, (i, err.max())

@@ -270,3 +270,14 @@ def test_pipelined_matches_serial(argus_mod):
     for kk in gh:
         np.testing.assert_array_equal(gh[kk], ref[3][1][kk])
     assert rc_h == ref[3][0]
+
+
+@pytest.mark.parametrize("N,M,d,seed", [(64, 4096, 1024, 111), (200, 20000, 1024, 112), (77, 9000, 832, 113),
+                                        (129, 5000, 960, 114), (33, 3000, 64, 115)])
+def test_wide_and_narrow_embeddings(argus_mod, N, M, d, seed):
+    """d > 768 (OpenCLIP-H d = 1024, C4): k-blocks 12.. of the prompt slice are read by
+    the MMA from shared memory, cache tiles stream through quarter-tile slots; d = 832
+    / 960 split unevenly over the quarters; d = 64 is a single k-block."""
+    p = gen.small_problem("C4", N=N, M=M, d=d, seed=seed)
+    g, tk, _ = run_case(argus_mod, p)
+    assert tk["max_score_err"] < 1e-4

@@ -251,11 +251,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      // end markers in the next two tile slots (one per MMA issuer; same reuse rule as
-      // a real tile)
+      // end markers in the next two tile slots (one per MMA issuer).  Before reusing
+      // tile-ring entry l % 8 the consumers of tile l - 8 must be done, which the release
+      // of an earlier real tile's first slot guarantees (that MMA needed the epilogue's
+      // release of a later tile).  SPT = 2: the slot a real tile l would use was last
+      // used by tile l - 2.  SPT = 4: every tile uses slot 0, and the marker tiles never
+      // fill it, so both markers wait for the last real tile's release of slot 0.
+      const int64_t l_end = l;
       for (int e = 0; e < 2; ++e, ++l) {
-        const int64_t u = SPT * l;
-        tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 2) & 1) ^ 1));
+        if (SPT == 2) {
+          const int64_t u = SPT * l;
+          tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 2) & 1) ^ 1));
+        } else if (l_end > 0) {
+          const int64_t u = SPT * (l_end - 1);
+          tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)((u >> 2) & 1));
+        }
         sm->tile_id[l & (INV_SLOTS - 1)] = -1;
         tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
       }

@@ -137,6 +137,7 @@ struct argus_router {
   uint8_t* h_outblk = nullptr;     // pinned mirror
   size_t outblk_bytes = 0;
   bool pending = false;            // async (_dev) work enqueued since the last argus_sync
+  bool serial_call = false;        // host-buffer call in progress: one stream with PDL, no event hops
   // F1 (policy, PASM, affinity window) and F3 (Eq. 3 workers)
   int32_t policy = 0;              // ARGUS_POLICY_SD / ARGUS_POLICY_PASM
   uint64_t seed = 0;
@@ -952,7 +953,7 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     return ARGUS_E_INVALID;
   r->pending = true;
   int32_t P = 0;
-  if (r->pipe) {  // prep / scan / tail on the internal streams (see the file header)
+  if (r->pipe && !r->serial_call) {  // prep / scan / tail on the internal streams (see the file header)
     const int q = (int)(r->seq & 1);
     CU_TRY(r, cudaEventRecord(r->ev_in[q], r->stream));  // prompts (and earlier inserts) are ready
     CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_in[q], 0));
@@ -1058,9 +1059,13 @@ int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const
   argus_route_extra dx{optimal_out ? reinterpret_cast<int32_t*>(D + o_ob) : nullptr,
                        worker_out ? reinterpret_cast<int32_t*>(D + o_wk) : nullptr,
                        handle_out ? reinterpret_cast<uint64_t*>(D + o_hd) : nullptr};
+  // the call is synchronous, so pipelining cannot overlap anything; everything was
+  // drained above, so the parity-0 buffers of the single-stream path are free
+  r->serial_call = true;
   rc = argus_route_batch_ex_dev(r, r->d_Xstage, N, quota, reinterpret_cast<int32_t*>(D + o_opt),
                                 reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
                                 reinterpret_cast<float*>(D + o_rh), D + o_st, &dx);
+  r->serial_call = false;
   if (rc) return rc;
   rc = argus_route_join(r, nullptr);
   if (rc) return rc;

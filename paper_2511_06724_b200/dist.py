@@ -10,14 +10,25 @@ process group, and max-over-ranks timing.  Tested with world_size=2 gloo on CPU
 from __future__ import annotations
 
 
-def stripe_owner(g: int, world: int) -> int:
+def cache_position(g: int, capacity: int = 0, evict: bool = False) -> int:
+    """Cache position of global id g: g itself, or g mod capacity for a ring-evicting
+    cache (argus_config.evict; capacity % world == 0)."""
+    return g % capacity if evict else g
+
+
+def stripe_owner(g: int, world: int, capacity: int = 0, evict: bool = False) -> int:
     """Rank holding global cache id g."""
-    return g % world
+    return cache_position(g, capacity, evict) % world
 
 
-def stripe_slot(g: int, world: int) -> int:
+def stripe_slot(g: int, world: int, capacity: int = 0, evict: bool = False) -> int:
     """Local row of global id g on its owner."""
-    return g // world
+    return cache_position(g, capacity, evict) // world
+
+
+def live_ids(M: int, capacity: int, evict: bool) -> range:
+    """Global ids held after M inserts: all of them, or the last `capacity` (ring)."""
+    return range(max(0, M - capacity), M) if evict else range(M)
 
 
 def local_rows(M: int, world: int, rank: int) -> int:

@@ -84,3 +84,50 @@ def test_ring_before_wrap_matches_plain_cache(argus_mod):
             outs.append(r.argus_route_batch(p.X, quota)[1])
     for key in ("option", "topk_idx", "topk_score", "quality"):
         np.testing.assert_array_equal(outs[0][key], outs[1][key])
+
+
+def test_ring_eviction_g_invariance(argus_mod):
+    """A wrapped ring cache striped over G = 1, 2, 4 routers (external collective
+    mode, one GPU): bit-identical outputs, top-k over the live ids, handles."""
+    import torch
+    argus = argus_mod
+    p = gen.small_problem("C2", N=90, M=7000, seed=306)
+    N, k, L, cap = 90, p.k, len(p.opts), 4096
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    handles = np.arange(7000, dtype=np.uint64) + np.uint64(1 << 40)
+    X = torch.from_numpy(p.X).cuda()
+    ref = None
+    for G in (1, 2, 4):
+        routers = [argus.Router(768, k, p.opts, p.W1, p.b1, p.W2, p.b2, capacity=cap, max_batch=N, rank=rk,
+                                world=G, evict=True) for rk in range(G)]
+        for r in routers:
+            r.argus_cache_insert_h(p.cache[:5000], handles[:5000])
+            r.argus_cache_insert_h(p.cache[5000:], handles[5000:])
+        keys = torch.zeros((G, N, k), dtype=torch.int64, device="cuda")
+        for rk, r in enumerate(routers):
+            r.argus_route_partial_dev(X, keys[rk])
+        for r in routers:
+            r.argus_sync()
+        outs = []
+        for r in routers:
+            o = dict(option=torch.empty(N, dtype=torch.int32, device="cuda"),
+                     topk_idx=torch.empty((N, k), dtype=torch.int32, device="cuda"),
+                     topk_score=torch.empty((N, k), dtype=torch.float32, device="cuda"),
+                     quality=torch.empty((N, L), dtype=torch.float32, device="cuda"),
+                     status=torch.empty(N, dtype=torch.uint8, device="cuda"))
+            r.argus_route_finish_dev(keys, G, N, quota, o["option"], o["topk_idx"], o["topk_score"],
+                                     o["quality"], o["status"])
+            r.argus_sync()
+            outs.append({kk: v.cpu().numpy() for kk, v in o.items()})
+            r.close()
+        for o in outs[1:]:
+            for kk in o:
+                np.testing.assert_array_equal(o[kk], outs[0][kk])
+        if ref is None:
+            ref = outs[0]
+        else:
+            for kk in ref:
+                np.testing.assert_array_equal(outs[0][kk], ref[kk])
+    live = np.arange(7000 - cap, 7000, dtype=np.uint32)
+    ref["topk_idx"] = ref["topk_idx"].view(np.uint32)
+    parity.check_topk(p.X, p.cache[7000 - cap:], k, ref["topk_idx"], ref["topk_score"], ids=live)

@@ -50,6 +50,23 @@ def _worker(rank, world, port, q):
             merged[i] = allix[i][o]
         ref_sc, ref_ix = oracle.scan_topk(p.X, p.cache, k)
         ok_topk = bool(np.array_equal(merged, ref_ix))
+        # ring-evicting cache (capacity 600 < M, wrapped): each rank holds the live ids
+        # whose position g mod 600 is in its stripe; merging the shards' candidates by
+        # (score desc, id asc) is the top-k over exactly the live set
+        cap = 600
+        live = np.array(list(adist.live_ids(M, cap, True)), np.uint32)
+        mine = np.array([g for g in live if adist.stripe_owner(int(g), world, cap, True) == rank], np.uint32)
+        slots = sorted(adist.stripe_slot(int(g), world, cap, True) for g in mine)
+        assert slots == list(range(len(mine)))              # dense local slots 0..cap/G-1
+        sc, ix = oracle.scan_topk(p.X, p.cache[mine], k, ids=mine)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (sc, ix))
+        allsc = np.concatenate([g[0] for g in gathered], axis=1)
+        allix = np.concatenate([g[1] for g in gathered], axis=1)
+        ref_sc, ref_ix = oracle.scan_topk(p.X, p.cache[live], k, ids=live)
+        for i in range(p.X.shape[0]):
+            o = np.lexsort((allix[i].astype(np.int64), -allsc[i]))[:k]
+            ok_topk = ok_topk and bool(np.array_equal(allix[i][o], ref_ix[i]))
         uid = adist.share_nccl_id(dist, rank, argus.argus_nccl_unique_id)
         uids = [None] * world
         dist.all_gather_object(uids, uid)

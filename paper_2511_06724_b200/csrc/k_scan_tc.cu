@@ -10,19 +10,23 @@
 //     handed out dynamically in chunks of CHUNK tiles (one atomic per chunk, fetched
 //     a chunk ahead), so CTAs that start late (SMs still busy with the previous
 //     batch's tail kernel) just take fewer chunks; CTAs of all slices sweep the
-//     cache in the same order, so slices > 1 re-hit each tile in L2;
+//     cache in the same order, so slices > 1 re-hit each tile in L2 (a lockstep
+//     window that forced this at 64 slices cost more in waiting than the HBM
+//     re-reads it saved: DESIGN.md §12);
 //   * the prompt slice is the UMMA A operand and lives in TMEM for the whole
-//     kernel (128 lanes x d/2 columns, loaded once with tcgen05.st);
+//     kernel (128 lanes x up to 384 columns, loaded once with tcgen05.st); for
+//     d > 768 k-blocks 12.. stay in shared memory (SS-mode MMAs);
 //   * cache tiles of 64 rows are the B operand: TMA (128-byte swizzle, L2
-//     evict-first) streams 64x64 bf16 boxes through a ring of 4 half-tile slots;
+//     evict-first for one slice) streams 64x64 bf16 boxes through a ring of 4
+//     slots (half tiles, or quarter tiles for d > 768);
 //   * tcgen05.mma.cta_group::1.kind::f16, M=128 (prompts) x N=64 (cache rows) x
-//     K=16, issued warp-uniformly (elect.sync inside the asm) into one of two TMEM
-//     accumulators, one tcgen05.commit per half tile (a commit costs ~250 issue
-//     cycles, an N=64 MMA ~32);
+//     K=16, issued warp-uniformly (elect.sync inside the asm) by two warps (even /
+//     odd tiles) into two TMEM accumulators, one tcgen05.commit per slot (a commit
+//     costs ~250 issue cycles, an N=64 MMA 32 pipe cycles);
 //   * epilogue: 8 warps, TMEM lane = prompt, each thread owns one prompt and one
 //     32-column half of every tile and keeps its top-k in registers behind a float
 //     threshold shared (monotonically) with the other lists of the same prompt.
-// Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator, 3 = idle,
+// Warp roles: 0 = TMA producer, 1 / 3 = MMA issuers, 2 = TMEM allocator,
 // 4..11 = Q loader + epilogue.
 #include <cstddef>
 #include <cstdlib>

@@ -125,7 +125,7 @@ struct argus_router {
   float* d_score = nullptr;        // [max_batch][k]
   uint32_t* d_idx = nullptr;       // [max_batch][k]
   float* d_rhat = nullptr;         // [max_batch][L]
-  uint8_t* d_pref = nullptr;       // [max_batch][L] rank of option v in pi_i
+  uint8_t* d_pref = nullptr;       // [max_batch][L] pi_i as a list of options
   uint8_t* d_ccount = nullptr;     // [max_batch]
   uint32_t* d_cmask = nullptr;     // [max_batch]
   uint8_t* d_status = nullptr;     // [max_batch]
@@ -895,7 +895,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.L = L;
   m.Lw = (L + 3) / 4 * 4;
   m.rhat = quality_dev ? quality_dev : r->d_rhat;
-  m.rankof = r->d_pref;
+  m.prefl = r->d_pref;
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)

@@ -21,10 +21,10 @@
 // tcgen05 tile.  W1x is pre-arranged at init in per-lane fragment order so each B
 // fragment is one coalesced 8-byte load.  In phase 2 one warp owns one prompt and
 // lane v owns option v (L <= 32): masks are ballots, the preference rank is a
-// 32-lane compare-count, stored as the inverse permutation rank_i(v) that phase 3
-// consumes.  Phase 3 walks the prompts in priority order in one warp with lane v
-// holding rem_v and rank_i(v): one REDUX.MIN per prompt picks "the first option of
-// pi_i with quota left".
+// 32-lane compare-count, scattered into the list pi_i that phase 3 consumes.  Phase 3
+// runs the serial dictatorship 32 prompts at a time in one warp: each lane takes the
+// first option of its pi_i with quota left, and the group commits up to the first
+// lane whose option the earlier lanes used up (at most N/32 + L group steps).
 #include <cstdio>
 
 #include "common.cuh"
@@ -140,10 +140,11 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
   __syncthreads();
 
   // serial dictatorship over staged chunks
-  int rem = lane < L ? a.quota[lane] : 0;  // warp 0 only
+  __shared__ int32_t rem_s[32];
+  if (tid < 32) rem_s[tid] = tid < L ? a.quota[tid] : 0;
   bool any_overflow = false;
   const int W = Lw / 4;
-  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.rankof);
+  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.prefl);
   for (int c0 = 0; c0 < N; c0 += CH) {
     const int n = min(CH, N - c0);
     for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
@@ -174,17 +175,43 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
     }
     __syncthreads();
     if (warp == 0) {
-      uint32_t nxt = lane < L ? rk_s[lane] : 0xFFu;
-      for (int t = 0; t < n; ++t) {
-        const uint32_t rk = nxt;
-        if (t + 1 < n) nxt = lane < L ? rk_s[(size_t)(t + 1) * Lw + lane] : 0xFFu;
-        const uint32_t cand = (rk != 0xFFu && rem > 0) ? rk : 0xFFu;
-        const uint32_t best = __reduce_min_sync(0xffffffffu, cand);
-        const bool mine = best != 0xFFu && cand == best;  // positions are distinct: one lane
-        rem -= mine ? 1 : 0;
-        const uint32_t who = __ballot_sync(0xffffffffu, mine);  // off the loop-carried chain
-        if (lane == 0) opt_s[t] = who ? (uint8_t)(__ffs(who) - 1) : (uint8_t)0x80;
-        any_overflow |= (who == 0);
+      // Serial dictatorship, 32 prompts at a time.  Each lane takes the first option of
+      // its pi_i that had quota left when the group started; the group's choices are
+      // exactly the sequential ones up to the first lane whose option was used up by
+      // earlier lanes of the group (running count >= remaining quota).  Those lanes
+      // commit, the rest restart with the new quotas.  An option runs out at most once,
+      // so a batch takes at most N/32 + L group steps.
+      uint32_t avail = __ballot_sync(0xffffffffu, lane < L && rem_s[lane] > 0);
+#pragma unroll 1
+      for (int t = 0; t < n;) {
+        const int j = t + lane;
+        int choice = 0xFF;  // no admissible option with quota left: overflow
+        if (j < n) {
+          const uint8_t* row = rk_s + (size_t)j * Lw;
+#pragma unroll 1
+          for (int r = 0; r < Lw; ++r) {
+            const int o = row[r];
+            if (o == 0xFF) break;
+            if ((avail >> o) & 1u) {
+              choice = o;
+              break;
+            }
+          }
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, choice);
+        const int before = __popc(peers & ((1u << lane) - 1u));
+        const bool ok = j >= n || choice == 0xFF || before < rem_s[choice];
+        const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+        const int take = min(bad ? __ffs(bad) - 1 : 32, n - t);  // >= 1: lane 0 is always ok
+        __syncwarp();
+        if (lane < take) {
+          opt_s[j] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
+          if (choice != 0xFF) atomicSub(&rem_s[choice], 1);
+          any_overflow |= choice == 0xFF;
+        }
+        __syncwarp();
+        avail = __ballot_sync(0xffffffffu, lane < L && rem_s[lane] > 0);
+        t += take;
       }
     }
     __syncthreads();
@@ -199,7 +226,7 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
     }
     __syncthreads();
   }
-  if (tid == 0 && any_overflow) atomicOr(a.flags, FLAG_OVERFLOW);
+  if (warp == 0 && __any_sync(0xffffffffu, any_overflow) && lane == 0) atomicOr(a.flags, FLAG_OVERFLOW);
 }
 
 // ------------------------------------------------------------------ F1: PASM sampling
@@ -487,12 +514,10 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
                           (ru > rr || (ru == rr && (pu > pth || (pu == pth && u < lane))));
       rank += before ? 1 : 0;
     }
-    if (act) {
-      a.rhat[(int64_t)i * L + lane] = rr;
-      a.rankof[(int64_t)i * a.Lw + lane] = adm ? (uint8_t)rank : (uint8_t)0xFF;  // position of v in pi_i
-    } else if (lane < a.Lw) {
-      a.rankof[(int64_t)i * a.Lw + lane] = 0xFF;
-    }
+    if (act) a.rhat[(int64_t)i * L + lane] = rr;
+    // pi_i as a list: admissible option v at its position, 0xFF after the last
+    if (adm) a.prefl[(int64_t)i * a.Lw + rank] = (uint8_t)lane;
+    if (lane < a.Lw && lane >= __popc(amask)) a.prefl[(int64_t)i * a.Lw + lane] = 0xFF;
     // optimal option o_i: the compliant option with the largest p_th, then
     // the larger r, then the lower index (DESIGN R18); option 0 is always compliant
     float kp = cmp ? pth : -INFINITY, kr = cmp ? rr : -INFINITY;

@@ -96,9 +96,9 @@ struct TailArgs {
   const float* pth;          // [L]
   const float* gate;         // [L]
   float delta;
-  int32_t N, d, k, H, L, Lw; // Lw = L rounded up to 4 (rankof row stride)
+  int32_t N, d, k, H, L, Lw; // Lw = L rounded up to 4 (prefl row stride)
   float* rhat;               // [N][L] out
-  uint8_t* rankof;           // [N][Lw] position of option v in pi_i (0xFF: not admissible)
+  uint8_t* prefl;            // [N][Lw] pi_i as a list: option at position r (0xFF past |A_i|)
   uint8_t* ccount;           // [N] |C_i|
   uint32_t* cmask;           // [N] compliance mask
   // A6

@@ -281,3 +281,27 @@ def test_wide_and_narrow_embeddings(argus_mod, N, M, d, seed):
     p = gen.small_problem("C4", N=N, M=M, d=d, seed=seed)
     g, tk, _ = run_case(argus_mod, p)
     assert tk["max_score_err"] < 1e-4
+
+
+@pytest.mark.parametrize("seed", [131, 132, 133, 134])
+def test_assignment_random_quotas(argus_mod, seed):
+    """The tail's parallel deferred-acceptance rounds must equal the oracle's serial
+    dictatorship (O10) bit-exactly under arbitrary quotas: zeros, a few large ones,
+    sum below N (overflow) and far above N."""
+    p = gen.small_problem("C5", N=700, M=6000, seed=seed)
+    rng = np.random.default_rng(seed)
+    L = len(p.opts)
+    with make_router(argus_mod, p) as r:
+        r.argus_cache_insert(p.cache)
+        for trial in range(6):
+            q = rng.integers(0, 80, L).astype(np.int32)
+            q[rng.random(L) < 0.3] = 0
+            if trial == 0:
+                q[:] = 0
+                q[0] = 700                    # everything on the full model
+            if trial == 1:
+                q = (q * 10).astype(np.int32)  # slack everywhere
+            rc, g = r.argus_route_batch(p.X, q)
+            rep = parity.check_replay(g, p.opts, q)
+            assert rc == rep["rc"]
+            parity.invariants(g, p.opts, q)

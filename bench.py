@@ -271,25 +271,44 @@ def main():
     total_prompts = prompts  # every rank routes the same prompts; the batch is the job's unit
     value = total_prompts / (ms_max / 1e3)
 
-    # ---- e2e through the host-buffer ABI call
-    e2e_steps = args.e2e_steps or min(args.steps, 200)
+    # ---- e2e through the public host-buffer API: argus_route_batch_async, the call of
+    # a serving loop (pinned host prompts -> device, the whole path, outputs -> pinned
+    # host buffers, every step; up to two calls in flight), timed on the router's stream
+    e2e_steps = args.e2e_steps or args.steps
     Xh = [x.numpy() for x in X_pin]
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt).pin_memory().numpy()
+
+    outs_h = [dict(option=pinned((n,), torch.int32), topk_idx=pinned((n, k), torch.int32).view(np.uint32),
+                   topk_score=pinned((n, k), torch.float32), quality=pinned((n, L), torch.float32),
+                   status=pinned((n,), torch.uint8)) for n in sizes]
+    for t in range(min(4, NT)):  # warm the async path
+        r.argus_route_wait(r.argus_route_batch_async(Xh[t], quotas[t], outs_h[t]))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e2e_prompts, h2d, d2h = 0, 0, 0
     with torch.cuda.stream(stream):
         e0.record(stream)
+        last = None
         for t in range(e2e_steps):
             b = t % NT
-            r.argus_route_batch(Xh[b], quotas[b])
+            last = r.argus_route_batch_async(Xh[b], quotas[b], outs_h[b])
             n = sizes[b]
             e2e_prompts += n
             h2d += n * d * 4
-            d2h += n * (4 + k * 8 + L * 4 + 1)
+            d2h += n * (4 + k * 8 + L * 4 + 1) + 4
+        r.argus_route_wait(last)  # every call's outputs are in host memory
         e1.record(stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    # the synchronous call, for reference (one batch at a time, nothing overlaps)
+    sync_steps = min(e2e_steps, 100)
+    s0 = time.perf_counter()
+    for t in range(sync_steps):
+        r.argus_route_batch(Xh[t % NT], quotas[t % NT])
+    sync_pps = sum(sizes[t % NT] for t in range(sync_steps)) / (time.perf_counter() - s0)
     if world > 1:
         e2e_ms = adist.max_over_ranks(dist, e2e_ms, dev)
 
@@ -373,7 +392,10 @@ def main():
         },
         "e2e": {"value": round(e2e_prompts / (e2e_ms / 1e3), 1), "unit": "prompts/s",
                 "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
-                "steps": e2e_steps, "api": "argus_route_batch (host buffers)"},
+                "steps": e2e_steps,
+                "api": "argus_route_batch_async (pinned host buffers; H2D of the prompts and D2H of all outputs "
+                       "inside every step; up to two calls in flight), then argus_route_wait",
+                "sync_call_prompts_per_s": round(sync_pps, 1)},
         "gpu_launches": int(launches),
         "roofline": {
             "kernel": "scan (K1+K2 fused cosine scan + top-k)",

@@ -179,6 +179,26 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N,
                           uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                           uint8_t* status_dev);
 
+/* Asynchronous host-buffer route: the call of a serving loop.  Enqueues the copy of
+ * prompts (host fp32 [N][d]) to the device, the whole path, and the copies of the
+ * outputs back into the caller's host buffers (same meaning as argus_route_batch;
+ * quality_out / status_out may be NULL), then returns at once with *ticket set to
+ * an increasing call id.  All buffers must stay alive and untouched until
+ * argus_route_wait(r, *ticket) returns; use pinned (page-locked) host memory, or the
+ * copies run synchronously.  With cfg.pipeline = 1 consecutive calls overlap (the
+ * tail of one with the scan of the next).  A call waits (on the host) for the call
+ * issued two calls before it to finish.  Returns ARGUS_OK once enqueued or an
+ * argument error; the call's own result comes from argus_route_wait. */
+int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                            int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
+                            uint8_t* status_out, int64_t* ticket);
+
+/* Wait until the asynchronous call `ticket` (and every earlier one) has delivered its
+ * outputs; return its result (ARGUS_OK, ARGUS_W_OVERFLOW, ARGUS_E_INVALID for an
+ * invalid prompt).  Each ticket's result can be collected once; waiting for a later
+ * ticket first implicitly collects the earlier ones (ARGUS_E_INVALID afterwards). */
+int argus_route_wait(argus_router* r, int64_t ticket);
+
 /* Sharded pipeline pieces (external collective mode and tests).
  * partial: A1-A3 on this rank's shard -> keys_dev [N][k] uint64 (sorted desc;
  *          key = ord(score) << 32 | (0xFFFFFFFF - g), 0 = empty).

@@ -34,7 +34,7 @@ SYMBOLS = (
     "argus_get_stream", "argus_profile_enable", "argus_profile_read", "argus_route_destroy",
     "argus_strerror", "argus_solve_allocation", "argus_oda_pasm", "argus_pasm_degradation", "argus_set_policy",
     "argus_affinity_histogram", "argus_set_workers", "argus_get_queues", "argus_route_batch_ex",
-    "argus_route_batch_ex_dev", "argus_cache_insert_h",
+    "argus_route_batch_ex_dev", "argus_cache_insert_h", "argus_route_batch_async", "argus_route_wait",
 )
 STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
@@ -97,6 +97,8 @@ def _load():
         "argus_route_batch_ex": [P, P, I32, P, P, P, P, P, P, P],
         "argus_route_batch_ex_dev": [P, P, I32, P, P, P, P, P, P, P],
         "argus_cache_insert_h": [P, P, P, I64, P],
+        "argus_route_batch_async": [P, P, I32, P, P, P, P, P, P, P],
+        "argus_route_wait": [P, I64],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -310,6 +312,27 @@ class Router:
         return _check(_lib.argus_route_batch_ex_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
                                                     _p(topk_idx), _p(topk_score), _p(quality), _p(status),
                                                     C.byref(ex)), "argus_route_batch_ex_dev")
+
+    def argus_route_batch_async(self, prompts, quota, out):
+        """Enqueue one batch from (pinned) host memory; outputs land in the arrays of
+        `out` (option, topk_idx, topk_score, optional quality / status), which must
+        stay alive until argus_route_wait(ticket).  Returns the ticket."""
+        N = int(prompts.shape[0])
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
+        t = C.c_int64(-1)
+        _check(_lib.argus_route_batch_async(self._h, _p(prompts), N, _p(quota), _p(out["option"]),
+                                            _p(out["topk_idx"]), _p(out["topk_score"]), _p(out.get("quality")),
+                                            _p(out.get("status")), C.byref(t)), "argus_route_batch_async")
+        self._async_keep = getattr(self, "_async_keep", {})
+        self._async_keep[t.value] = (prompts, quota, out)   # keep the buffers alive
+        return t.value
+
+    def argus_route_wait(self, ticket) -> int:
+        rc = _check(_lib.argus_route_wait(self._h, C.c_int64(int(ticket))), "argus_route_wait")
+        keep = getattr(self, "_async_keep", {})
+        for t in [x for x in keep if x <= ticket]:
+            del keep[t]
+        return rc
 
     def argus_cache_insert_h(self, emb, handles=None) -> int:
         emb = np.ascontiguousarray(emb, np.float32).reshape(-1, self.d)

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <map>
 #include <vector>
 
 #include "../../include/argus.h"
@@ -138,6 +139,16 @@ struct argus_router {
   size_t outblk_bytes = 0;
   bool pending = false;            // async (_dev) work enqueued since the last argus_sync
   bool serial_call = false;        // host-buffer call in progress: one stream with PDL, no event hops
+  // asynchronous host-buffer calls (argus_route_batch_async): per-parity device
+  // staging of the prompts and outputs, per-parity flags, completion events
+  uint32_t* flags_cur = nullptr;   // flags word the kernels of the current call OR into
+  float* d_Xasync[2] = {nullptr, nullptr};
+  uint8_t* d_oasync[2] = {nullptr, nullptr};
+  uint32_t* h_fasync = nullptr;    // [2] pinned flag words
+  cudaEvent_t ev_async[2] = {nullptr, nullptr};
+  int64_t async_ticket[2] = {-1, -1};  // ticket whose D2H the parity slot carries (-1: none)
+  int64_t next_ticket = 0;
+  std::map<int64_t, int> async_rc;     // harvested results of finished tickets
   // F1 (policy, PASM, affinity window) and F3 (Eq. 3 workers)
   int32_t policy = 0;              // ARGUS_POLICY_SD / ARGUS_POLICY_PASM
   uint64_t seed = 0;
@@ -393,11 +404,14 @@ int argus_route_destroy(argus_router* r) {
                   r->d_score, r->d_idx, r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option,
                   r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1], r->d_cdf, r->d_plast,
                   r->d_aff, r->d_wlist, r->d_wcount, r->d_wtime, r->d_queue, r->d_optimal, r->d_worker,
-                  r->d_handle};
+                  r->d_handle, r->d_Xasync[0], r->d_Xasync[1], r->d_oasync[0], r->d_oasync[1]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
   if (r->h_outblk) cudaFreeHost(r->h_outblk);
+  if (r->h_fasync) cudaFreeHost(r->h_fasync);
+  for (cudaEvent_t e : r->ev_async)
+    if (e) cudaEventDestroy(e);
   if (r->d_outblk) cudaFree(r->d_outblk);
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
@@ -538,6 +552,15 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_queue, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_optimal, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_handle, (size_t)std::max<int64_t>(c.capacity, 1)));
+  for (int q = 0; q < 2; ++q) {
+    TRY_RC(dalloc(r, &r->d_Xasync[q], (size_t)c.max_batch * d));
+    TRY_RC(dalloc(r, &r->d_oasync[q], 16 + 16 * 8 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1)));
+    if (cudaEventCreateWithFlags(&r->ev_async[q], cudaEventDisableTiming) != cudaSuccess) {
+      argus_route_destroy(r);
+      return ARGUS_E_CUDA;
+    }
+  }
+  if (cudaMallocHost((void**)&r->h_fasync, 2 * sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   TRY_RC(dalloc(r, &r->d_worker, (size_t)c.max_batch));
   r->outblk_bytes = 16 + 16 * 8 + (size_t)c.max_batch * (4 + 16 * (size_t)k + 4 * (size_t)L + 1 + 8);
   TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
@@ -781,7 +804,8 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
     StageScope sc(r, ARGUS_STAGE_PREP, s_prep);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q], r->d_flags,
+    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q],
+                        r->flags_cur ? r->flags_cur : r->d_flags,
                         s_prep, !pipelined);
     LAUNCHED(r);
   }
@@ -902,7 +926,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   for (int v = 0; v < 32; ++v) m.quota[v] = (v < L && quota) ? quota[v] : 0;
   m.option_out = option_out_dev ? option_out_dev : r->d_option;
   m.status = status_dev ? status_dev : r->d_status;
-  m.flags = r->d_flags;
+  m.flags = r->flags_cur ? r->flags_cur : r->d_flags;
   m.policy = r->policy;
   m.pasm_cdf = r->d_cdf;
   m.pasm_last = r->d_plast;
@@ -1089,6 +1113,84 @@ int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
   return ARGUS_OK;
+}
+
+// ------------------------------------------------------------------ asynchronous host-buffer calls
+static int flags_rc(uint32_t fl) {
+  if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
+  if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
+  return ARGUS_OK;
+}
+
+// Finish the call carried by parity slot q (if any): wait for its D2H, keep its rc.
+static int async_harvest(argus_router* r, int q) {
+  if (r->async_ticket[q] < 0) return ARGUS_OK;
+  CU_TRY(r, cudaEventSynchronize(r->ev_async[q]));
+  r->async_rc[r->async_ticket[q]] = flags_rc(r->h_fasync[q]);
+  r->async_ticket[q] = -1;
+  return ARGUS_OK;
+}
+
+int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
+                            int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,
+                            uint8_t* status_out, int64_t* ticket) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  const bool root = r->cfg.rank == 0 || !nccl_mode(r);
+  if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota) || !option_out || !ticket ||
+      (r->cfg.k > 0 && (!topk_idx || !topk_score)))
+    return ARGUS_E_INVALID;
+  if (root && !prompts) return ARGUS_E_INVALID;
+  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
+  const int q = (int)(r->next_ticket & 1);
+  rc = async_harvest(r, q);  // the slot's previous call (two calls ago) must have landed
+  if (rc) return rc;
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_opt = 16, o_idx = al(o_opt + 4 * (size_t)N), o_sc = al(o_idx + 4 * (size_t)N * k),
+               o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L);
+  uint8_t* D = r->d_oasync[q];
+  uint32_t* dflags = reinterpret_cast<uint32_t*>(D);
+  CU_TRY(r, cudaMemsetAsync(dflags, 0, 4, r->stream));
+  if (root)
+    CU_TRY(r, cudaMemcpyAsync(r->d_Xasync[q], prompts, sizeof(float) * N * d, cudaMemcpyHostToDevice, r->stream));
+  r->flags_cur = dflags;
+  rc = argus_route_batch_ex_dev(r, r->d_Xasync[q], N, quota, reinterpret_cast<int32_t*>(D + o_opt),
+                                reinterpret_cast<uint32_t*>(D + o_idx), reinterpret_cast<float*>(D + o_sc),
+                                quality_out ? reinterpret_cast<float*>(D + o_rh) : nullptr, D + o_st, nullptr);
+  r->flags_cur = nullptr;
+  if (rc) return rc;
+  // results back to the caller's buffers, ordered after this call's tail
+  cudaStream_t s = (r->pipe && r->tail_inflight[(r->seq - 1) & 1]) ? r->tail_stream : r->stream;
+  CU_TRY(r, cudaMemcpyAsync(option_out, D + o_opt, 4 * (size_t)N, cudaMemcpyDeviceToHost, s));
+  if (k > 0) {
+    CU_TRY(r, cudaMemcpyAsync(topk_idx, D + o_idx, 4 * (size_t)N * k, cudaMemcpyDeviceToHost, s));
+    CU_TRY(r, cudaMemcpyAsync(topk_score, D + o_sc, 4 * (size_t)N * k, cudaMemcpyDeviceToHost, s));
+  }
+  if (quality_out) CU_TRY(r, cudaMemcpyAsync(quality_out, D + o_rh, 4 * (size_t)N * L, cudaMemcpyDeviceToHost, s));
+  if (status_out) CU_TRY(r, cudaMemcpyAsync(status_out, D + o_st, (size_t)N, cudaMemcpyDeviceToHost, s));
+  CU_TRY(r, cudaMemcpyAsync(r->h_fasync + q, dflags, 4, cudaMemcpyDeviceToHost, s));
+  CU_TRY(r, cudaEventRecord(r->ev_async[q], s));
+  r->async_ticket[q] = r->next_ticket;
+  *ticket = r->next_ticket++;
+  return ARGUS_OK;
+}
+
+int argus_route_wait(argus_router* r, int64_t ticket) {
+  if (!r) return ARGUS_E_INVALID;
+  if (r->poisoned) return ARGUS_E_STATE;
+  if (ticket < 0 || ticket >= r->next_ticket) return ARGUS_E_INVALID;
+  for (int q = 0; q < 2; ++q)
+    if (r->async_ticket[q] >= 0 && r->async_ticket[q] <= ticket) {
+      const int rc = async_harvest(r, q);
+      if (rc) return rc;
+    }
+  auto it = r->async_rc.find(ticket);
+  if (it == r->async_rc.end()) return ARGUS_E_INVALID;  // already collected
+  const int rc = it->second;
+  r->async_rc.erase(r->async_rc.begin(), std::next(it));  // older tickets are implicitly collected
+  return rc;
 }
 
 // ------------------------------------------------------------------ F1 / F3 router state

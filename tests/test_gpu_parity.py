@@ -305,3 +305,55 @@ def test_assignment_random_quotas(argus_mod, seed):
             rep = parity.check_replay(g, p.opts, q)
             assert rc == rep["rc"]
             parity.invariants(g, p.opts, q)
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_async_host_calls_match_sync(argus_mod, pipeline):
+    """argus_route_batch_async (pinned host buffers, H2D + path + D2H enqueued, up to
+    two calls in flight) returns exactly what the synchronous host call returns, and
+    each ticket carries its own result code (overflow, invalid prompt)."""
+    import torch
+    argus = argus_mod
+    p = gen.small_problem("C2", N=300, M=20000, seed=141)
+    k, L = p.k, len(p.opts)
+    sizes = [64, 300, 1, 129, 300, 77, 200, 33]
+    rng = np.random.default_rng(9)
+    batches = [np.ascontiguousarray(p.X[rng.choice(300, n, replace=False)]) for n in sizes]
+    quotas = [oracle.quota_from_fractions(p.fractions, n) for n in sizes]
+    quotas[3] = np.maximum(quotas[3] - 20, 0).astype(np.int32)     # overflow in call 3
+    bad = 5
+    batches[bad] = batches[bad].copy()
+    batches[bad][3, 7] = np.nan                                       # invalid prompt in call 5
+    with make_router(argus, p, max_batch=300, pipeline=pipeline) as r:
+        r.argus_cache_insert(p.cache)
+        ref = []
+        for b, (x, q) in enumerate(zip(batches, quotas)):
+            if b == bad:
+                with pytest.raises(argus.ArgusError):
+                    r.argus_route_batch(x, q)
+                ref.append(None)
+            else:
+                ref.append(r.argus_route_batch(x, q))
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        tickets, outs = [], []
+        for x, q in zip(batches, quotas):
+            n = x.shape[0]
+            o = dict(option=pin(np.full(n, -7, np.int32)), topk_idx=pin(np.zeros((n, k), np.uint32)),
+                     topk_score=pin(np.zeros((n, k), np.float32)), quality=pin(np.zeros((n, L), np.float32)),
+                     status=pin(np.zeros(n, np.uint8)))
+            tickets.append(r.argus_route_batch_async(pin(x), q, o))
+            outs.append(o)
+        rcs = []
+        for t in tickets:
+            try:
+                rcs.append(r.argus_route_wait(t))
+            except argus.ArgusError as e:
+                rcs.append(e.code)
+    for b, (rf, o, rc) in enumerate(zip(ref, outs, rcs)):
+        if b == bad:
+            assert rc == argus.ARGUS_E_INVALID
+            continue
+        assert rc == rf[0], (b, rc, rf[0])
+        for key in ("option", "topk_idx", "topk_score", "quality", "status"):
+            np.testing.assert_array_equal(o[key], rf[1][key])
+    assert rcs[3] == 1   # ARGUS_W_OVERFLOW

@@ -166,6 +166,9 @@ struct argus_router {
   int32_t* d_optimal = nullptr;    // [max_batch] host-path staging of o_i
   int32_t* d_worker = nullptr;     // [max_batch] host-path staging of worker ids
   CUtensorMap tmap_c;              // TMA descriptor of the bf16 cache shard (64x64 boxes, SW128)
+  CUtensorMap tmap_c32;            // same shard, 32x64 boxes (half tiles of the CTA-pair scan)
+  bool pair_scan = true;           // N > 128 on CTA pairs (ARGUS_NO_PAIR=1 disables)
+  int tail_ysplit = 1;             // CTAs per prompt block of a pipelined tail (ARGUS_TAIL_YSPLIT)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   // stage profiling (argus_profile_*)
   bool prof = false;
@@ -479,6 +482,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     r->own_stream = true;
   }
   r->pipe = c.pipeline != 0 && c.world == 1;
+  r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
+  if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
   if (r->pipe) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -568,6 +573,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (cudaMallocHost((void**)&r->h_outblk, r->outblk_bytes) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (cudaMallocHost((void**)&r->h_flags, sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   if (!make_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d, 64) ||
+      !make_tmap(&r->tmap_c32, r->d_Cb, r->cap_local + 256, d, 32) ||
       !make_tmap(&r->tmap_q[0], r->d_Xb[0], r->n_pad_max, d, 128) ||
       !make_tmap(&r->tmap_q[1], r->d_Xb[1], r->n_pad_max, d, 128)) {
     argus_route_destroy(r);
@@ -846,11 +852,15 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.partial = r->d_partial[q];
   a.gthr = r->d_gthr[q];
   a.ctr = r->d_ctr[q];
-  a.P = scan_plan_ranges(a.m_local, N, r->num_sms);
+  const bool pair = r->pair_scan && scan_pair_supported(d, N);
+  a.P = pair ? scan_pair_plan(a.m_local, N, r->num_sms) : scan_plan_ranges(a.m_local, N, r->num_sms);
   if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
-    launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
+    if (pair)
+      launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined);
+    else
+      launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
   }
   LAUNCHED(r);
   *P_out = a.P;
@@ -951,7 +961,10 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.worker_out = ex ? ex->worker : nullptr;
   {
     StageScope sc(r, ARGUS_STAGE_TAIL, s);
-    launch_tail(m, r->tail_smem, s, pdl);
+    // a pipelined tail overlaps the next scan: one CTA per prompt block keeps its SM
+    // footprint small; a tail on the critical path spreads over H/32 CTAs per block
+    const int ysplit = s == r->tail_stream ? r->tail_ysplit : r->cfg.hidden / 32;
+    launch_tail(m, r->tail_smem, s, pdl, ysplit);
   }
   LAUNCHED(r);
   r->batch_seq++;

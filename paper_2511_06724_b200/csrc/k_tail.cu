@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smraw);        // [PB][RS]
   float* red = reinterpret_cast<float*>(smraw + (size_t)PB * RS * 2);  // [TW][PB*32]
   float* ss = red + TW * PB * 32;                                     // [PB][k]
-  const int pb = blockIdx.x, cc = blockIdx.y;
+  const int pb = blockIdx.x;
   const int i0 = pb * PB;
   const int nP = min(PB, a.N - i0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -311,16 +311,6 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     const int p = idx / (d / 8), c = idx - p * (d / 8);
     cp_async16(xs + p * RS + c * 8, reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d) + c);
   }
-  // per-thread epilogue constants of layer 1
-  float w1s_r[2][8], b1_r[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int j = cc * 32 + ((tid + u * TT) & 31);
-    b1_r[u] = __ldg(a.b1 + j);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
-  }
-
   if (ARGUS_TAIL_TIMING) U[0] = gtimer();
   // ---- phase M: merge the P lists of k keys of each prompt of the block.  All of the
   // block's keys (P slabs of 16 prompts x k, contiguous per list) arrive with one burst of
@@ -365,7 +355,7 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     if (pl < nP && hl < k) {
       const uint64_t key = mk[pl][hl];
       ss[pl * k + hl] = key_score(key);
-      if (cc == 0) {
+      if (blockIdx.y == 0) {
         const uint32_t age = key_id(key);  // 0xFFFFFFFF for an empty slot (M < k)
         a.topk_idx[(int64_t)i * k + hl] = key == 0 ? 0xFFFFFFFFu : a.id_base + age;
         a.topk_score[(int64_t)i * k + hl] = key_score(key);
@@ -383,8 +373,20 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   __syncthreads();
   if (ARGUS_TAIL_TIMING) T[2] = gtimer();
 
-  // ---- phase 1: hidden units [32 cc, 32 cc + 32), warp w takes a 1/8 slice of d
-  {
+  // ---- phase 1: hidden units [32 cc, 32 cc + 32) for cc = blockIdx.y, blockIdx.y +
+  // gridDim.y, ...; warp w takes a 1/8 slice of d.  gridDim.y = H / 32 spreads a block
+  // over H / 32 CTAs (lowest latency); gridDim.y = 1 keeps the block in one CTA, so the
+  // candidate lists are merged once, not H / 32 times, and a pipelined tail occupies
+  // few SMs while the next batch's scan starts.
+  for (int cc = blockIdx.y; cc < H / 32; cc += gridDim.y) {
+    float w1s_r[2][8], b1_r[2];  // per-thread epilogue constants of this chunk
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = cc * 32 + ((tid + u * TT) & 31);
+      b1_r[u] = __ldg(a.b1 + j);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
+    }
     const int g = lane >> 2, t = lane & 3;
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
     const int RSW = RS / 2;
@@ -421,19 +423,20 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) rw[(g + (e >> 1) * 8) * 32 + nt * 8 + 2 * t + (e & 1)] = acc[nt][e];
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {  // PB * 32 = 2 * TT: reduce split-K partials in a fixed order
-    const int e = tid + u * TT;
-    const int row = e >> 5, j = cc * 32 + (e & 31);
-    float z = 0.f;
+    for (int u = 0; u < 2; ++u) {  // PB * 32 = 2 * TT: reduce split-K partials in a fixed order
+      const int e = tid + u * TT;
+      const int row = e >> 5, j = cc * 32 + (e & 31);
+      float z = 0.f;
 #pragma unroll
-    for (int w = 0; w < TW; ++w) z = __fadd_rn(z, red[w * PB * 32 + e]);
+      for (int w = 0; w < TW; ++w) z = __fadd_rn(z, red[w * PB * 32 + e]);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < k) z = __fmaf_rn(w1s_r[u][q], ss[row * k + q], z);
-    a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, b1_r[u]), 0.f);
+      for (int q = 0; q < 8; ++q)
+        if (q < k) z = __fmaf_rn(w1s_r[u][q], ss[row * k + q], z);
+      a.hbuf[(int64_t)(i0 + row) * H + j] = fmaxf(__fadd_rn(z, b1_r[u]), 0.f);
+    }
+    __syncthreads();  // red is reused by the next chunk
   }
   if (ARGUS_TAIL_TIMING) T[3] = gtimer();
   __threadfence();
@@ -607,13 +610,14 @@ void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStr
   k_prep_w1_frag<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(w1, d, k, H, reinterpret_cast<uint2*>(Wf));
 }
 
-void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl) {
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl, int ysplit) {
   static size_t attr_set = 0;
   if (smem > attr_set) {
     cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = smem;
   }
-  const dim3 grid((a.N + PB - 1) / PB, a.H / 32);
+  const int ys = ysplit < 1 ? 1 : (ysplit > a.H / 32 ? a.H / 32 : ysplit);
+  const dim3 grid((a.N + PB - 1) / PB, ys);
   launch_pdl_opt(pdl, k_tail, grid, dim3(TT), smem, s, a);
 }
 

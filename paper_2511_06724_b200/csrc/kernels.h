@@ -66,6 +66,13 @@ bool scan_supported(int d);
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q, cudaStream_t s,
                  bool pdl = true);
 
+// K1+K2 on CTA pairs (tcgen05.mma.cta_group::2) for N > 128 and d <= 768:
+// grid = 2 * ceil(N / 256) * P CTAs in clusters of two, P from scan_pair_plan.
+int scan_pair_plan(int64_t m_local, int32_t N, int num_sms);
+bool scan_pair_supported(int d, int32_t N);
+void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q, cudaStream_t s,
+                      bool pdl = true);
+
 // K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
 // decoding ids / scores.
 void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint64_t* keys_out,
@@ -125,7 +132,9 @@ struct TailArgs {
 // K3+K4 (+K5 on one GPU): merge, predictor, A5 and the assignment in one launch.
 // pdl = false when the tail's producer is on another stream (pipelined mode):
 // griddepcontrol.wait only orders against the previous kernel of the same stream.
-void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl);
+// ysplit = CTAs per 16-prompt block (hidden units split H/32 ways at most): H/32 for
+// the lowest latency, 1 for the smallest SM footprint (pipelined mode).
+void launch_tail(const TailArgs& a, size_t smem, cudaStream_t s, bool pdl, int ysplit);
 size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max);
 // init: W1x (columns [0,d) of w1 [H][d+k]) -> bf16 fragment order [H*d] bf16
 void launch_prep_w1_frag(const float* w1, int d, int k, int H, void* Wf, cudaStream_t s);

@@ -273,7 +273,7 @@ def main():
 
     # ---- e2e through the public host-buffer API: argus_route_batch_async, the call of
     # a serving loop (pinned host prompts -> device, the whole path, outputs -> pinned
-    # host buffers, every step; up to two calls in flight), timed on the router's stream
+    # host buffers, every step; up to four calls in flight), timed on the router's stream
     e2e_steps = args.e2e_steps or args.steps
     Xh = [x.numpy() for x in X_pin]
 
@@ -394,7 +394,7 @@ def main():
                 "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
                 "steps": e2e_steps,
                 "api": "argus_route_batch_async (pinned host buffers; H2D of the prompts and D2H of all outputs "
-                       "inside every step; up to two calls in flight), then argus_route_wait",
+                       "inside every step; up to four calls in flight), then argus_route_wait",
                 "sync_call_prompts_per_s": round(sync_pps, 1)},
         "gpu_launches": int(launches),
         "roofline": {

@@ -187,7 +187,7 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N,
  * argus_route_wait(r, *ticket) returns; use pinned (page-locked) host memory, or the
  * copies run synchronously.  With cfg.pipeline = 1 consecutive calls overlap (the
  * tail of one with the scan of the next).  A call waits (on the host) for the call
- * issued two calls before it to finish.  Returns ARGUS_OK once enqueued or an
+ * issued four calls before it to finish.  Returns ARGUS_OK once enqueued or an
  * argument error; the call's own result comes from argus_route_wait. */
 int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, const int32_t* quota,
                             int32_t* option_out, uint32_t* topk_idx, float* topk_score, float* quality_out,

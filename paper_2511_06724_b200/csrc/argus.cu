@@ -142,11 +142,12 @@ struct argus_router {
   // asynchronous host-buffer calls (argus_route_batch_async): per-parity device
   // staging of the prompts and outputs, per-parity flags, completion events
   uint32_t* flags_cur = nullptr;   // flags word the kernels of the current call OR into
-  float* d_Xasync[2] = {nullptr, nullptr};
-  uint8_t* d_oasync[2] = {nullptr, nullptr};
-  uint32_t* h_fasync = nullptr;    // [2] pinned flag words
-  cudaEvent_t ev_async[2] = {nullptr, nullptr};
-  int64_t async_ticket[2] = {-1, -1};  // ticket whose D2H the parity slot carries (-1: none)
+  static constexpr int NASYNC = 4;     // asynchronous calls in flight
+  float* d_Xasync[NASYNC] = {};
+  uint8_t* d_oasync[NASYNC] = {};
+  uint32_t* h_fasync = nullptr;    // [NASYNC] pinned flag words
+  cudaEvent_t ev_async[NASYNC] = {};
+  int64_t async_ticket[NASYNC] = {-1, -1, -1, -1};  // ticket whose D2H the slot carries (-1: none)
   int64_t next_ticket = 0;
   std::map<int64_t, int> async_rc;     // harvested results of finished tickets
   // F1 (policy, PASM, affinity window) and F3 (Eq. 3 workers)
@@ -407,7 +408,8 @@ int argus_route_destroy(argus_router* r) {
                   r->d_score, r->d_idx, r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option,
                   r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1], r->d_cdf, r->d_plast,
                   r->d_aff, r->d_wlist, r->d_wcount, r->d_wtime, r->d_queue, r->d_optimal, r->d_worker,
-                  r->d_handle, r->d_Xasync[0], r->d_Xasync[1], r->d_oasync[0], r->d_oasync[1]};
+                  r->d_handle, r->d_Xasync[0], r->d_Xasync[1], r->d_Xasync[2], r->d_Xasync[3], r->d_oasync[0],
+                  r->d_oasync[1], r->d_oasync[2], r->d_oasync[3]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -557,7 +559,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_queue, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_optimal, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_handle, (size_t)std::max<int64_t>(c.capacity, 1)));
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < argus_router::NASYNC; ++q) {
     TRY_RC(dalloc(r, &r->d_Xasync[q], (size_t)c.max_batch * d));
     TRY_RC(dalloc(r, &r->d_oasync[q], 16 + 16 * 8 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1)));
     if (cudaEventCreateWithFlags(&r->ev_async[q], cudaEventDisableTiming) != cudaSuccess) {
@@ -565,7 +567,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
       return ARGUS_E_CUDA;
     }
   }
-  if (cudaMallocHost((void**)&r->h_fasync, 2 * sizeof(uint32_t)) != cudaSuccess) { argus_route_destroy(r); return ARGUS_E_CUDA; }
+  if (cudaMallocHost((void**)&r->h_fasync, argus_router::NASYNC * sizeof(uint32_t)) != cudaSuccess) {
+    argus_route_destroy(r);
+    return ARGUS_E_CUDA;
+  }
   TRY_RC(dalloc(r, &r->d_worker, (size_t)c.max_batch));
   r->outblk_bytes = 16 + 16 * 8 + (size_t)c.max_batch * (4 + 16 * (size_t)k + 4 * (size_t)L + 1 + 8);
   TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
@@ -1157,8 +1162,8 @@ int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, co
   if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
-  const int q = (int)(r->next_ticket & 1);
-  rc = async_harvest(r, q);  // the slot's previous call (two calls ago) must have landed
+  const int q = (int)(r->next_ticket % argus_router::NASYNC);
+  rc = async_harvest(r, q);  // the slot's previous call (NASYNC calls ago) must have landed
   if (rc) return rc;
   auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
   const size_t o_opt = 16, o_idx = al(o_opt + 4 * (size_t)N), o_sc = al(o_idx + 4 * (size_t)N * k),
@@ -1194,7 +1199,7 @@ int argus_route_wait(argus_router* r, int64_t ticket) {
   if (!r) return ARGUS_E_INVALID;
   if (r->poisoned) return ARGUS_E_STATE;
   if (ticket < 0 || ticket >= r->next_ticket) return ARGUS_E_INVALID;
-  for (int q = 0; q < 2; ++q)
+  for (int q = 0; q < argus_router::NASYNC; ++q)
     if (r->async_ticket[q] >= 0 && r->async_ticket[q] <= ticket) {
       const int rc = async_harvest(r, q);
       if (rc) return rc;

@@ -10,6 +10,8 @@
 // therefore pulls half the cache bytes through TMA; with one slice per CTA the
 // multi-slice scans were capped by the chip's TMA/L2->SM throughput (~10 TB/s of
 // tile traffic at N = 256..512), and a 256-prompt batch now reads each tile once.
+// For d > 768 (KBV = 16) k-blocks 12.. of each CTA's prompts stay in its shared
+// memory and those MMAs take A by descriptor, as in k_scan_tc.cu.
 //
 // Roles (both CTAs unless noted): warp 0 = TMA producer (the leader also fetches
 // the pair's tile schedule and publishes every tile id into the peer's ring through
@@ -36,15 +38,22 @@ constexpr int TN = 64;                       // cache rows per tile (MMA N)
 constexpr int HR = 32;                       // rows of each tile held by each CTA
 constexpr int TM = 128;                      // prompts per CTA (M = 256 per pair)
 constexpr int KBLK = 64;
-constexpr int KB_MAX = 12;                   // d <= 768 (A fully in TMEM)
+constexpr int KB_TMEM = 12;                  // k-blocks of A in TMEM (d <= 768)
+constexpr int KB_MAX = 16;                   // d <= 1024: k-blocks 12.. of A stay in shared memory
 constexpr int BOX_BYTES = HR * KBLK * 2;     // 4 KB: 32 rows x 64 bf16
 constexpr int QBOX_BYTES = TM * KBLK * 2;    // 16 KB prompt box
-constexpr int NSLOT = 8;                     // half-tile slots: 4 tiles in flight
-constexpr int SLOT_BOXES = KB_MAX / 2;
-constexpr int SLOT_BYTES = SLOT_BOXES * BOX_BYTES;  // 24 KB
+constexpr int NSLOT = 8;                     // tile-part slots
 constexpr int REGION_BYTES = 192 * 1024;
-static_assert(NSLOT * SLOT_BYTES <= REGION_BYTES, "ring");
-static_assert(KB_MAX * QBOX_BYTES <= REGION_BYTES, "prompt staging");
+static_assert(KB_TMEM * QBOX_BYTES <= REGION_BYTES, "prompt staging");
+// KBV = 12: half-tile slots of 6 boxes (24 KB), 4 tiles in flight.  KBV = 16: the A
+// tail (64 KB) first, then quarter-tile slots of 4 boxes (16 KB), 2 tiles in flight.
+template <int KBV>
+struct PShape {
+  static constexpr int SPT = KBV == 12 ? 2 : 4;
+  static constexpr int SLOT_BYTES = (KBV / SPT) * BOX_BYTES;
+  static constexpr int RING0 = (KBV - KB_TMEM) * QBOX_BYTES;
+  static_assert(RING0 + NSLOT * SLOT_BYTES <= REGION_BYTES, "ring");
+};
 constexpr int THREADS = 384;
 constexpr int EPI_WARPS = 8;
 constexpr int ACC_COL0 = 384;
@@ -64,6 +73,7 @@ struct PairSmem {
   uint64_t qfull;               // this CTA's prompt boxes landed in shared memory
   uint64_t qlocal;              // this CTA's prompt slice is in TMEM: the region is free
   uint64_t qpair;               // leader: both slices are in TMEM (16 warp arrivals)
+  uint64_t atail;               // leader, KBV = 16: both CTAs' A tails landed (tx of both)
   uint64_t tsched[INV_SLOTS];   // peer: the leader published tile_id[l % 8]
   uint64_t invfull[INV_SLOTS];  // inv_c of tile l landed (publishes tile_id[l % 8] locally)
   int64_t tile_id[INV_SLOTS];
@@ -74,14 +84,17 @@ struct PairSmem {
 static_assert(offsetof(PairSmem, invc) % 16 == 0, "bulk-copy / float4 destination");
 static_assert(sizeof(PairSmem) <= SCRATCH_OFF, "barriers fit before the scratch");
 
-template <int KMAX>
+template <int KMAX, int KBV>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_pair(const __grid_constant__ CUtensorMap tmap_c32, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
                 int pslices, int64_t n_tiles, int l2mode) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using SH = PShape<KBV>;
+  constexpr int SPT = SH::SPT;
   PairSmem* sm = reinterpret_cast<PairSmem*>(ring + (size_t)REGION_BYTES);
-  const uint32_t ring_s = tc::smem_u32(ring);
+  const uint32_t region_s = tc::smem_u32(ring);  // prompt staging, then [A tail | ring]
+  const uint32_t ring_s = region_s + (uint32_t)SH::RING0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = tc::cluster_ctarank();  // 0 = leader (issues the MMAs)
   const bool leader = crank == 0;
@@ -105,6 +118,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::mbar_init(tc::smem_u32(&sm->qfull), 1);
     tc::mbar_init(tc::smem_u32(&sm->qlocal), EPI_WARPS);
     tc::mbar_init(tc::smem_u32(&sm->qpair), 2 * EPI_WARPS);
+    tc::mbar_init(tc::smem_u32(&sm->atail), 1);
     for (int s = 0; s < INV_SLOTS; ++s) {
       tc::mbar_init(tc::smem_u32(&sm->tsched[s]), 1);
       tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
@@ -125,32 +139,40 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ======================= TMA producers
     if (lane == 0) {
+      const int KBT = KB < KB_TMEM ? KB : KB_TMEM;
       const uint32_t qb = tc::smem_u32(&sm->qfull);
-      tc::mbar_arrive_expect_tx(qb, (uint32_t)(KB * QBOX_BYTES));
-      for (int kb = 0; kb < KB; ++kb)
-        tc::tma_load_2d(ring_s + (uint32_t)(kb * QBOX_BYTES), &tmap_q, qb, kb * KBLK, pbase);
+      tc::mbar_arrive_expect_tx(qb, (uint32_t)(KBT * QBOX_BYTES));
+      for (int kb = 0; kb < KBT; ++kb)
+        tc::tma_load_2d(region_s + (uint32_t)(kb * QBOX_BYTES), &tmap_q, qb, kb * KBLK, pbase);
       tc::mbar_wait(tc::smem_u32(&sm->qlocal), 0);  // region free again
+      if (KBV > KB_TMEM) {  // A tail: k-blocks 12.. of this CTA's prompts, counted on the leader's atail
+        const uint32_t ab_local = tc::smem_u32(&sm->atail);
+        if (leader) tc::mbar_arrive_expect_tx(ab_local, (uint32_t)(2 * (KB - KB_TMEM) * QBOX_BYTES));
+        const uint32_t ab = tc::mapa(ab_local, 0);
+        for (int kb = KB_TMEM; kb < KB; ++kb)
+          tc::tma_load_2d_pair(region_s + (uint32_t)((kb - KB_TMEM) * QBOX_BYTES), &tmap_q, ab, kb * KBLK, pbase,
+                               tc::policy_evict_normal());
+      }
       const int l2m = l2mode & 15;
       const uint64_t pol = l2m == 0 ? tc::policy_evict_first()
                                     : (l2m == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
-      const int kb_half[2] = {(KB + 1) / 2, KB / 2};
-      // the leader's full barriers, as cluster addresses (the peer's loads signal them)
       auto issue = [&](int64_t l, int64_t t) {
-        for (int hh = 0; hh < 2; ++hh) {
-          const int64_t u = 2 * l + hh;
+#pragma unroll
+        for (int hh = 0; hh < SPT; ++hh) {
+          const int64_t u = SPT * l + hh;
           const int sl = (int)(u & (NSLOT - 1));
           tc::mbar_wait(tc::smem_u32(&sm->empty[sl]), (uint32_t)(((u >> 3) & 1) ^ 1));
+          const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
           const uint32_t fb_local = tc::smem_u32(&sm->full[sl]);
-          if (leader) tc::mbar_arrive_expect_tx(fb_local, (uint32_t)(2 * kb_half[hh] * BOX_BYTES));
+          if (leader) tc::mbar_arrive_expect_tx(fb_local, (uint32_t)(2 * (kb1 - kb0) * BOX_BYTES));
           if (hh == 0) {  // the tile's inverse norms, for this CTA's epilogue (all 64 rows)
             const uint32_t ib = tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]);
             tc::mbar_arrive_expect_tx(ib, TN * 4);
             tc::bulk_load_hint(tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][0]), a.inv_c + t * TN, TN * 4, ib, pol);
           }
-          const uint32_t fb = tc::mapa(fb_local, 0);
-          const int kb0 = hh ? kb_half[0] : 0;
-          for (int j = 0; j < kb_half[hh]; ++j)
-            tc::tma_load_2d_pair(ring_s + (uint32_t)(sl * SLOT_BYTES + j * BOX_BYTES), &tmap_c32, fb,
+          const uint32_t fb = tc::mapa(fb_local, 0);  // the leader's full barrier counts both halves
+          for (int j = 0; j < kb1 - kb0; ++j)
+            tc::tma_load_2d_pair(ring_s + (uint32_t)(sl * SH::SLOT_BYTES + j * BOX_BYTES), &tmap_c32, fb,
                                  (kb0 + j) * KBLK, (int32_t)(t * TN + (int64_t)crank * HR), pol);
         }
       };
@@ -167,7 +189,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // ring entry l % 8 is free in both CTAs once slot 2l's previous tile (l - 4)
             // was consumed; the wait inside issue() for hh = 0 guarantees it, so publish
             // after that wait: do the hh = 0 wait first
-            const int64_t u = 2 * l;
+            const int64_t u = SPT * l;
             tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 3) & 1) ^ 1));
             sm->tile_id[l & (INV_SLOTS - 1)] = t;
             tc::st_async_s64(tc::mapa(tc::smem_u32(&sm->tile_id[l & (INV_SLOTS - 1)]), 1), t,
@@ -175,10 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             issue(l, t);
           }
         }
-        // two end markers (one per MMA issuer); the slot a real tile l would use was last
-        // used by tile l - 4, a real tile or none
+        // two end markers (one per MMA issuer); the first slot a tile l would use was
+        // last used by tile l - 8 / SPT (4 or 2 tiles back): a real tile or none
         for (int e = 0; e < 2; ++e, ++l) {
-          const int64_t u = 2 * l;
+          const int64_t u = SPT * l;
           tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 3) & 1) ^ 1));
           sm->tile_id[l & (INV_SLOTS - 1)] = -1;
           tc::st_async_s64(tc::mapa(tc::smem_u32(&sm->tile_id[l & (INV_SLOTS - 1)]), 1), -1,
@@ -207,9 +229,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ======================= MMA issuers (leader): M = 256 (both CTAs' prompts) x N = 64
     constexpr uint32_t IDESC = tc::idesc_bf16_f32(2 * TM, TN);
     tc::mbar_wait(tc::smem_u32(&sm->qpair), 0);
+    if (KBV > KB_TMEM) tc::mbar_wait(tc::smem_u32(&sm->atail), 0);
     tc::fence_after();
-    const int kb_half0 = (KB + 1) / 2;
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
+    const uint64_t abase = tc::desc_kmajor_sw128(region_s);  // A tail (KBV = 16)
     for (int64_t l = warp == 1 ? 0 : 1;; l += 2) {
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       if (sm->tile_id[l & (INV_SLOTS - 1)] < 0) break;
@@ -218,20 +241,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::fence_after();
       const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int64_t u = 2 * l + hh;
+      for (int hh = 0; hh < SPT; ++hh) {
+        const int64_t u = SPT * l + hh;
         const int sl = (int)(u & (NSLOT - 1));
         tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 3) & 1));
         tc::fence_after();
-        const int kb0 = hh ? kb_half0 : 0;
-        const int nkb = hh ? KB - kb_half0 : kb_half0;
-        const uint64_t dslot = dbase + (uint64_t)((sl * SLOT_BYTES) >> 4);
-        for (int j = 0; j < nkb; ++j) {
+        const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
+        const uint64_t dslot = dbase + (uint64_t)((sl * SH::SLOT_BYTES) >> 4);
+        for (int j = 0; j < kb1 - kb0; ++j) {
           const int kb = kb0 + j;
+          if (KBV == KB_TMEM || kb < KB_TMEM) {
 #pragma unroll
-          for (int kk = 0; kk < KBLK / 16; ++kk)
-            tc::mma_ts_pair_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
-                                 dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
+            for (int kk = 0; kk < KBLK / 16; ++kk)
+              tc::mma_ts_pair_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
+                                   dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
+          } else {  // A tail from shared memory (each CTA holds its 128 rows at this offset)
+#pragma unroll
+            for (int kk = 0; kk < KBLK / 16; ++kk)
+              tc::mma_ss_pair_warp(d_tmem, abase + (uint64_t)(((kb - KB_TMEM) * QBOX_BYTES + kk * 32) >> 4),
+                                   dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, 1u);
+          }
         }
         tc::mma_commit_pair_warp(tc::smem_u32(&sm->empty[sl]), (uint16_t)0x3);  // slot free in both CTAs
       }
@@ -248,8 +277,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     {
       tc::mbar_wait(tc::smem_u32(&sm->qfull), 0);
       const int sw = p_local & 7;
-      for (int c = h; c < KB; c += 2) {
-        const uint32_t row = ring_s + (uint32_t)(c * QBOX_BYTES + p_local * 128);
+      const int KBT = KB < KB_TMEM ? KB : KB_TMEM;
+      for (int c = h; c < KBT; c += 2) {
+        const uint32_t row = region_s + (uint32_t)(c * QBOX_BYTES + p_local * 128);
         uint32_t r[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -272,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     const bool active = p < a.N;
     const float iq = a.inv_q[p];
-    const uint32_t scratch = ring_s + (uint32_t)(REGION_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
+    const uint32_t scratch = region_s + (uint32_t)(REGION_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;
@@ -355,13 +385,13 @@ bool scan_pair_supported(int d, int32_t N) {
   return d % KBLK == 0 && d / KBLK <= KB_MAX && slices >= 2 && slices % 2 == 0;
 }
 
-template <int KMAX>
+template <int KMAX, int KBV>
 static cudaError_t launch_pair_variant(bool pdl, dim3 grid, cudaStream_t s, const CUtensorMap& tc32,
                                        const CUtensorMap& tq, const ScanArgs& a, int pslices, int64_t n_tiles,
                                        int l2mode) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scan_pair<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(k_scan_pair<KMAX, KBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -381,11 +411,11 @@ static cudaError_t launch_pair_variant(bool pdl, dim3 grid, cudaStream_t s, cons
   static bool told = false;
   if (!told && getenv("ARGUS_DEBUG")) {
     int nc = -1;
-    cudaOccupancyMaxActiveClusters(&nc, (const void*)k_scan_pair<KMAX>, &cfg);
+    cudaOccupancyMaxActiveClusters(&nc, (const void*)k_scan_pair<KMAX, KBV>, &cfg);
     fprintf(stderr, "argus: pair scan grid %u CTAs, max co-resident 2-CTA clusters %d\n", grid.x, nc);
     told = true;
   }
-  return cudaLaunchKernelEx(&cfg, k_scan_pair<KMAX>, tc32, tq, a, pslices, n_tiles, l2mode);
+  return cudaLaunchKernelEx(&cfg, k_scan_pair<KMAX, KBV>, tc32, tq, a, pslices, n_tiles, l2mode);
 }
 
 void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q, cudaStream_t s,
@@ -400,10 +430,14 @@ void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUte
     l2env = e ? atoi(e) : -1;
   }
   const int l2mode = l2env >= 0 ? l2env : (pslices == 1 ? 0 : 1);
-  if (a.k <= 4)
-    launch_pair_variant<4>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
-  else
-    launch_pair_variant<8>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  const bool wide = a.d / KBLK > KB_TMEM;
+  if (a.k <= 4) {
+    if (wide) launch_pair_variant<4, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+    else launch_pair_variant<4, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  } else {
+    if (wide) launch_pair_variant<8, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+    else launch_pair_variant<8, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  }
 }
 
 }  // namespace argus

@@ -144,13 +144,15 @@ def test_determinism(argus_mod):
         np.testing.assert_array_equal(outs[0][key], outs[1][key])
 
 
-def test_g_invariance_striped_shards(argus_mod):
+@pytest.mark.parametrize("N", [70, 256])
+def test_g_invariance_striped_shards(argus_mod, N):
     """Outputs are bit-identical for G = 1, 2, 4 striped shards:
-    G routers on one GPU in external-collective mode, keys concatenated here."""
+    G routers on one GPU in external-collective mode, keys concatenated here.
+    N = 256 runs the CTA-pair scan on every shard."""
     import torch
     argus = argus_mod
-    p = gen.small_problem("C1", N=70, M=6001, seed=71)
-    N, k, L = 70, p.k, len(p.opts)
+    p = gen.small_problem("C1", N=N, M=6001, seed=71)
+    k, L = p.k, len(p.opts)
     quota = oracle.quota_from_fractions(p.fractions, N)
     X = torch.from_numpy(p.X).cuda()
     ref = None

@@ -857,15 +857,25 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.partial = r->d_partial[q];
   a.gthr = r->d_gthr[q];
   a.ctr = r->d_ctr[q];
-  const bool pair = r->pair_scan && scan_pair_supported(d, N);
-  a.P = pair ? scan_pair_plan(a.m_local, N, r->num_sms) : scan_plan_ranges(a.m_local, N, r->num_sms);
-  if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
+  bool pair = r->pair_scan && scan_pair_supported(d, N);
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
-    if (pair)
-      launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined);
-    else
+    if (pair) {
+      a.P = scan_pair_plan(a.m_local, N, r->num_sms);
+      if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
+      if (launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined) != cudaSuccess) {
+        // cluster launch refused (configuration, not a device fault): one slice per CTA from now on
+        cudaGetLastError();
+        r->pair_scan = false;
+        pair = false;
+        if (getenv("ARGUS_DEBUG")) fprintf(stderr, "argus: CTA-pair scan unavailable, using one slice per CTA\n");
+      }
+    }
+    if (!pair) {
+      a.P = scan_plan_ranges(a.m_local, N, r->num_sms);
+      if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;
       launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
+    }
   }
   LAUNCHED(r);
   *P_out = a.P;

@@ -418,8 +418,8 @@ static cudaError_t launch_pair_variant(bool pdl, dim3 grid, cudaStream_t s, cons
   return cudaLaunchKernelEx(&cfg, k_scan_pair<KMAX, KBV>, tc32, tq, a, pslices, n_tiles, l2mode);
 }
 
-void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q, cudaStream_t s,
-                      bool pdl) {
+cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q,
+                             cudaStream_t s, bool pdl) {
   const int pslices = (a.N + 2 * TM - 1) / (2 * TM);
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   const dim3 grid(2 * pslices * a.P);
@@ -431,13 +431,11 @@ void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUte
   }
   const int l2mode = l2env >= 0 ? l2env : (pslices == 1 ? 0 : 1);
   const bool wide = a.d / KBLK > KB_TMEM;
-  if (a.k <= 4) {
-    if (wide) launch_pair_variant<4, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
-    else launch_pair_variant<4, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
-  } else {
-    if (wide) launch_pair_variant<8, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
-    else launch_pair_variant<8, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
-  }
+  if (a.k <= 4)
+    return wide ? launch_pair_variant<4, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
+                : launch_pair_variant<4, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  return wide ? launch_pair_variant<8, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
+              : launch_pair_variant<8, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
 }
 
 }  // namespace argus

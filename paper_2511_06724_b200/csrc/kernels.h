@@ -70,8 +70,10 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap
 // grid = 2 * ceil(N / 256) * P CTAs in clusters of two, P from scan_pair_plan.
 int scan_pair_plan(int64_t m_local, int32_t N, int num_sms);
 bool scan_pair_supported(int d, int32_t N);
-void launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q, cudaStream_t s,
-                      bool pdl = true);
+// Returns the launch error (e.g. no TPC can host a 2-CTA cluster); the caller then
+// runs the one-slice-per-CTA kernel instead.
+cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q,
+                             cudaStream_t s, bool pdl = true);
 
 // K5: merge P lists of k keys per prompt -> keys [N][k] (desc), optionally
 // decoding ids / scores.

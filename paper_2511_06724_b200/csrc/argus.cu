@@ -567,10 +567,12 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
       return ARGUS_E_CUDA;
     }
   }
-  if (cudaMallocHost((void**)&r->h_fasync, argus_router::NASYNC * sizeof(uint32_t)) != cudaSuccess) {
+  // [NASYNC] flag words read back + one constant zero word
+  if (cudaMallocHost((void**)&r->h_fasync, (argus_router::NASYNC + 1) * sizeof(uint32_t)) != cudaSuccess) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
+  for (int q = 0; q <= argus_router::NASYNC; ++q) r->h_fasync[q] = 0u;
   TRY_RC(dalloc(r, &r->d_worker, (size_t)c.max_batch));
   r->outblk_bytes = 16 + 16 * 8 + (size_t)c.max_batch * (4 + 16 * (size_t)k + 4 * (size_t)L + 1 + 8);
   TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
@@ -1180,7 +1182,9 @@ int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, co
                o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L);
   uint8_t* D = r->d_oasync[q];
   uint32_t* dflags = reinterpret_cast<uint32_t*>(D);
-  CU_TRY(r, cudaMemsetAsync(dflags, 0, 4, r->stream));
+  // zero the call's flag word with a 4-byte copy (a copy-engine transfer, unlike a
+  // memset kernel, takes no SM away from the scan in flight)
+  CU_TRY(r, cudaMemcpyAsync(dflags, r->h_fasync + argus_router::NASYNC, 4, cudaMemcpyHostToDevice, r->stream));
   if (root)
     CU_TRY(r, cudaMemcpyAsync(r->d_Xasync[q], prompts, sizeof(float) * N * d, cudaMemcpyHostToDevice, r->stream));
   r->flags_cur = dflags;

@@ -845,6 +845,10 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   ScanArgs a{};
   a.head = (uint32_t)ring_head(r);
   a.capg = r->cfg.evict ? (uint32_t)r->cfg.capacity : 0u;
+  {
+    static const int win = getenv("ARGUS_PAIR_WINDOW") ? atoi(getenv("ARGUS_PAIR_WINDOW")) : 0;
+    a.window = win;
+  }
   a.Xb = r->d_Xb[q];
   a.inv_q = r->d_invq[q];
   a.Cb = r->d_Cb;

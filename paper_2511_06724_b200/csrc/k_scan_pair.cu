@@ -180,9 +180,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         int* ctr = a.ctr + pslice;
         int64_t l = 0;
         int64_t c = atomicAdd(ctr, 1);
+        int since = 0;
         for (;;) {
           const int64_t t0 = c * CHUNK;
           if (t0 >= n_tiles) break;
+          // optional lockstep window across pair slices (a.window chunks; 0 = off): keeps
+          // the pair slices' sweeps within what L2 holds (experiment knob)
+          if (a.window > 0 && pslices > 1 && ++since >= 4) {
+            since = 0;
+            const int64_t n_chunks = (n_tiles + CHUNK - 1) / CHUNK;
+            for (;;) {
+              int64_t lo = n_chunks;
+              for (int ps = 0; ps < pslices; ++ps) {
+                const int64_t cs = *reinterpret_cast<volatile int*>(a.ctr + ps);
+                lo = cs < lo ? cs : lo;
+              }
+              if (c <= lo + a.window) break;
+              __nanosleep(256);
+            }
+          }
           c = atomicAdd(ctr, 1);
           const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
           for (int64_t t = t0; t < t1; ++t, ++l) {

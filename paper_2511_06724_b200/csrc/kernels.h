@@ -46,6 +46,7 @@ struct ScanArgs {
   uint64_t* gthr;            // [n_pad] per-prompt shared top-k threshold key (zeroed by K6)
   int32_t* ctr;              // [MAX_SLICES] per-slice tile-chunk work counters (zeroed by K6)
   uint32_t head, capg;       // ring eviction: oldest live cache position, capacity (0, 0 when not wrapped)
+  int32_t window;            // pair scan: max chunks a pair slice may lead the slowest (0 = off)
 };
 constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts
 

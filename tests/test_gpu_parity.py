@@ -75,11 +75,13 @@ def test_gates_off_and_stress(argus_mod):
     assert len(np.unique(g["option"])) > 3
 
 
-def test_empty_cache_and_m_less_than_k(argus_mod):
-    p = gen.small_problem("C1", N=10, M=0, seed=31)
+@pytest.mark.parametrize("N", [10, 200, 300])
+def test_empty_cache_and_m_less_than_k(argus_mod, N):
+    """N = 200 runs the CTA-pair scan, N = 300 three single-CTA slices."""
+    p = gen.small_problem("C1", N=N, M=0, seed=31)
     g, _, _ = run_case(argus_mod, p, check_e2e=False)
     assert np.all(g["topk_idx"] == 0xFFFFFFFF) and np.all(g["topk_score"] == -1.0)
-    p = gen.small_problem("C1", N=10, M=3, seed=32)
+    p = gen.small_problem("C1", N=N, M=3, seed=32)
     g, _, _ = run_case(argus_mod, p)
     assert np.all(g["topk_idx"][:, 3] == 0xFFFFFFFF)
 

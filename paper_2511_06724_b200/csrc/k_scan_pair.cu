@@ -179,28 +179,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (leader) {
         int* ctr = a.ctr + pslice;
         int64_t l = 0;
-        int64_t c = atomicAdd(ctr, 1);
+        // tile-granular counter: CHUNK tiles per grab, single tiles for the last two
+        // chunks per pair of the pair slice (see k_scan_tc.cu)
+        const int64_t tail_tiles = (int64_t)(gridDim.x / (2 * pslices)) * CHUNK * 2;
+        int csz = n_tiles > tail_tiles ? CHUNK : 1;
+        int64_t c = atomicAdd(ctr, csz);
         int since = 0;
         for (;;) {
-          const int64_t t0 = c * CHUNK;
+          const int64_t t0 = c;
           if (t0 >= n_tiles) break;
           // optional lockstep window across pair slices (a.window chunks; 0 = off): keeps
           // the pair slices' sweeps within what L2 holds (experiment knob)
           if (a.window > 0 && pslices > 1 && ++since >= 4) {
             since = 0;
-            const int64_t n_chunks = (n_tiles + CHUNK - 1) / CHUNK;
             for (;;) {
-              int64_t lo = n_chunks;
+              int64_t lo = n_tiles;
               for (int ps = 0; ps < pslices; ++ps) {
                 const int64_t cs = *reinterpret_cast<volatile int*>(a.ctr + ps);
                 lo = cs < lo ? cs : lo;
               }
-              if (c <= lo + a.window) break;
+              if (t0 <= lo + (int64_t)a.window * CHUNK) break;
               __nanosleep(256);
             }
           }
-          c = atomicAdd(ctr, 1);
-          const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
+          const int64_t t1 = t0 + csz < n_tiles ? t0 + csz : n_tiles;
+          csz = n_tiles - t1 > tail_tiles ? CHUNK : 1;
+          c = atomicAdd(ctr, csz);
           for (int64_t t = t0; t < t1; ++t, ++l) {
             // ring entry l % 8 is free in both CTAs once slot 2l's previous tile (l - 4)
             // was consumed; the wait inside issue() for hh = 0 guarantees it, so publish

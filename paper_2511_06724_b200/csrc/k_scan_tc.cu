@@ -164,15 +164,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     : (l2m == 1 ? tc::policy_evict_normal() : tc::policy_evict_last());
       int* ctr = a.ctr + slice;
       int64_t l = 0;
-      // static split (diagnostics): CTA `range` takes chunks [c_lo, c_hi) in order
-      const int64_t n_chunks = (n_tiles + CHUNK - 1) / CHUNK;
-      const int64_t c_lo = n_chunks * range / (gridDim.x / slices), c_hi = n_chunks * (range + 1) / (gridDim.x / slices);
-      int64_t c = l2mode >= 16 ? c_lo : atomicAdd(ctr, 1);
+      // Tiles are handed out by a per-slice counter (in tiles): CHUNK at a time, then
+      // one at a time for the last two chunks per CTA of the slice, so the CTAs of a
+      // slice finish within about one tile of each other.  The next grab is fetched a
+      // chunk ahead (the atomic's latency overlaps this chunk's loads).
+      const int64_t tail_tiles = (int64_t)(gridDim.x / slices) * CHUNK * 2;
+      int csz = n_tiles > tail_tiles ? CHUNK : 1;
+      int64_t c = atomicAdd(ctr, csz);
       for (;;) {
-        const int64_t t0 = c * CHUNK;
-        if (t0 >= n_tiles || (l2mode >= 16 && c >= c_hi)) break;
-        c = l2mode >= 16 ? c + 1 : atomicAdd(ctr, 1);  // next chunk: the latency overlaps this chunk's loads
-        const int64_t t1 = t0 + CHUNK < n_tiles ? t0 + CHUNK : n_tiles;
+        const int64_t t0 = c;
+        if (t0 >= n_tiles) break;
+        const int64_t t1 = t0 + csz < n_tiles ? t0 + csz : n_tiles;
+        csz = n_tiles - t1 > tail_tiles ? CHUNK : 1;
+        c = atomicAdd(ctr, csz);
         for (int64_t t = t0; t < t1; ++t, ++l) {
 #pragma unroll
           for (int hh = 0; hh < SPT; ++hh) {
@@ -406,7 +410,7 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
     const char* e = getenv("ARGUS_SCAN_L2");
     l2env = e ? atoi(e) : -1;
   }
-  static int stat = (getenv("ARGUS_SCAN_STATIC") ? 16 : 0) | (getenv("ARGUS_SCAN_1MMA") ? 32 : 0);
+  static int stat = getenv("ARGUS_SCAN_1MMA") ? 32 : 0;
   const int l2mode = (l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1)) | stat;
   const bool wide = a.d / KBLK > KB_TMEM;
   if (a.k <= 4) {

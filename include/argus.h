@@ -217,8 +217,10 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
  * synchronisation.  Errors: ARGUS_E_CUDA. */
 int argus_route_join(argus_router* r, void* stream);
 
-/* Wait for all of the router's work (both streams); return the deferred code of the enqueued work
- * (ARGUS_OK, ARGUS_W_OVERFLOW, ARGUS_E_INVALID) and clear it. */
+/* Wait for all of the router's work (every stream, including the result copies of
+ * asynchronous host calls); return the deferred code of the enqueued device-buffer
+ * work (ARGUS_OK, ARGUS_W_OVERFLOW, ARGUS_E_INVALID) and clear it.  Results of
+ * asynchronous calls stay available to argus_route_wait. */
 int argus_sync(argus_router* r);
 
 /* Largest-remainder integer quotas from load shares (host helper, O(L)):

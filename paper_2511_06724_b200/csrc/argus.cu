@@ -899,6 +899,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                        uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr);
+static int async_harvest(argus_router* r, int q);
 static int quota_ok(const argus_router* r, const int32_t* quota) {
   if (r->policy == ARGUS_POLICY_PASM) return 1;  // quotas are not used when sampling the PASM
   if (!quota) return 0;
@@ -1071,6 +1072,12 @@ int argus_sync(argus_router* r) {
   CU_TRY(r, cudaMemcpyAsync(r->h_flags, r->d_flags, 4, cudaMemcpyDeviceToHost, r->stream));
   CU_TRY(r, cudaMemsetAsync(r->d_flags, 0, 4, r->stream));
   CU_TRY(r, cudaStreamSynchronize(r->stream));
+  // asynchronous host calls: their result copies follow the tails; collect them too
+  // (their result codes stay available to argus_route_wait)
+  for (int q = 0; q < argus_router::NASYNC; ++q) {
+    rc = async_harvest(r, q);
+    if (rc) return rc;
+  }
   r->pending = false;
   const uint32_t fl = *r->h_flags;
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;

@@ -118,7 +118,7 @@ struct argus_router {
   __nv_bfloat16* d_Xb[2] = {nullptr, nullptr};  // [n_pad_max][d] per batch parity
   float* d_invq[2] = {nullptr, nullptr};     // [n_pad_max] per batch parity
   uint64_t* d_gthr[2] = {nullptr, nullptr};  // [n_pad_max] shared per-prompt scan threshold
-  int32_t* d_ctr[2] = {nullptr, nullptr};    // [MAX_SLICES] scan work counters
+  int32_t* d_ctr[2] = {nullptr, nullptr};    // [CTR_WORDS] scan work / visit counters
   uint64_t* d_partial[2] = {nullptr, nullptr};  // [P * N <= partial_lists][k] per batch parity
   int64_t partial_lists = 0;
   uint64_t* d_keys = nullptr;      // [max_batch][k]
@@ -170,6 +170,7 @@ struct argus_router {
   CUtensorMap tmap_c32;            // same shard, 32x64 boxes (half tiles of the CTA-pair scan)
   bool pair_scan = true;           // N > 128 on CTA pairs (ARGUS_NO_PAIR=1 disables)
   int tail_ysplit = 1;             // CTAs per prompt block of a pipelined tail (ARGUS_TAIL_YSPLIT)
+  bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   // stage profiling (argus_profile_*)
   bool prof = false;
@@ -486,6 +487,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   r->pipe = c.pipeline != 0 && c.world == 1;
   r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
+  r->migrate = getenv("ARGUS_NO_MIGRATE") == nullptr;
   if (r->pipe) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -529,7 +531,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_invc, (size_t)r->cap_local + 256));
   TRY_RC(dalloc(r, &r->d_Xstage, (size_t)stage_rows * d));
   // P lists per prompt with P <= num_sms / slices and N <= 128 * slices
-  r->partial_lists = std::max<int64_t>((int64_t)r->num_sms * 128, c.max_batch);
+  // lists per prompt x prompts: <= num_sms * 128 for the one-slice-per-CTA scan; the
+  // pair scan with migration adds MAX_VISITS slots per pair slice
+  // (home_max + MAX_VISITS) * N <= (num_sms / 2 / pslices + 1 + MAX_VISITS) * 256 * pslices
+  r->partial_lists = (int64_t)r->num_sms * 128 + (int64_t)(MAX_VISITS + 1) * (((int64_t)c.max_batch + 255) / 256 * 256);
   for (int q = 0; q < 2; ++q) {
     TRY_RC(dalloc(r, &r->d_Xb[q], (size_t)r->n_pad_max * d));
     TRY_RC(dalloc(r, &r->d_partial[q], (size_t)r->partial_lists * k));
@@ -537,7 +542,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   for (int q = 0; q < 2; ++q) {
     TRY_RC(dalloc(r, &r->d_invq[q], (size_t)r->n_pad_max));
     TRY_RC(dalloc(r, &r->d_gthr[q], (size_t)r->n_pad_max));
-    TRY_RC(dalloc(r, &r->d_ctr[q], MAX_SLICES));
+    TRY_RC(dalloc(r, &r->d_ctr[q], CTR_WORDS));
   }
   TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
@@ -824,7 +829,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   }
   if (!root) {
     CU_TRY(r, cudaMemsetAsync(r->d_gthr[q], 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
-    CU_TRY(r, cudaMemsetAsync(r->d_ctr[q], 0, sizeof(int32_t) * MAX_SLICES, r->stream));
+    CU_TRY(r, cudaMemsetAsync(r->d_ctr[q], 0, sizeof(int32_t) * CTR_WORDS, r->stream));
   }
   if (pipelined) {
     CU_TRY(r, cudaEventRecord(r->ev_prep[q], s_prep));
@@ -867,7 +872,23 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
     if (pair) {
-      a.P = scan_pair_plan(a.m_local, N, r->num_sms);
+      // With more pair slices than divide the SMs' pairs evenly, launch a pair on every
+      // TPC and let pairs whose slice runs dry continue another slice (list slots
+      // [home_max, home_max + MAX_VISITS) for migrants, zeroed here since some stay unused).
+      const int pslices = (N + 255) / 256;
+      const int clusters = r->num_sms / 2;
+      const int64_t n_tiles = (a.m_local + 63) / 64;
+      a.migrate = r->migrate && pslices >= 2 && clusters % pslices != 0 && n_tiles >= (int64_t)clusters * 16;
+      if (a.migrate) {
+        a.home_max = (clusters + pslices - 1) / pslices;
+        a.P = a.home_max + MAX_VISITS;
+        a.grid_ctas = 2 * clusters;
+        if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
+        CU_TRY(r, cudaMemsetAsync(r->d_partial[q], 0, sizeof(uint64_t) * (size_t)a.P * N * k, s_scan));
+      } else {
+        a.P = scan_pair_plan(a.m_local, N, r->num_sms);
+        a.home_max = a.P;
+      }
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
       if (launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined) != cudaSuccess) {
         // cluster launch refused (configuration, not a device fault): one slice per CTA from now on

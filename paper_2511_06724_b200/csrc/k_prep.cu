@@ -59,7 +59,7 @@ __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, in
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   pdl_wait();  // the previous batch's kernels may still read Xb / inv_q
-  if (blockIdx.x == 0 && threadIdx.x < MAX_SLICES) ctr[threadIdx.x] = 0;  // scan work counters
+  if (blockIdx.x == 0 && threadIdx.x < CTR_WORDS) ctr[threadIdx.x] = 0;  // scan work / visit counters
   if (warp >= n_pad) return;
   if (lane == 0) gthr[warp] = 0;  // the scan's shared per-prompt threshold starts empty
   if (warp >= N) {  // zero padding rows: score 0, never reported

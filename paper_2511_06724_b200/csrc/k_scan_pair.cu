@@ -84,6 +84,15 @@ struct PairSmem {
 static_assert(offsetof(PairSmem, invc) % 16 == 0, "bulk-copy / float4 destination");
 static_assert(sizeof(PairSmem) <= SCRATCH_OFF, "barriers fit before the scratch");
 
+// tile entry: tile (36 bits) | pair slice (8) | list slot (8) | epoch (11); -1 = end
+__device__ __forceinline__ int64_t pack_tile(int64_t t, int ps, int slot, int ep) {
+  return t | ((int64_t)ps << 36) | ((int64_t)slot << 44) | ((int64_t)ep << 52);
+}
+__device__ __forceinline__ int64_t tile_of(int64_t pk) { return pk & ((int64_t(1) << 36) - 1); }
+__device__ __forceinline__ int pslice_of(int64_t pk) { return (int)((pk >> 36) & 0xFF); }
+__device__ __forceinline__ int slot_of(int64_t pk) { return (int)((pk >> 44) & 0xFF); }
+__device__ __forceinline__ int epoch_of(int64_t pk) { return (int)(pk >> 52); }
+
 template <int KMAX, int KBV>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_pair(const __grid_constant__ CUtensorMap tmap_c32, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
@@ -177,42 +186,60 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       };
       if (leader) {
-        int* ctr = a.ctr + pslice;
+        // A tile entry carries the tile, the pair slice, the list slot and the epoch
+        // (pack_tile); consumers reload the prompt slice when the epoch changes.
+        int cur = pslice, slot = range, ep = 0;
         int64_t l = 0;
         // tile-granular counter: CHUNK tiles per grab, single tiles for the last two
         // chunks per pair of the pair slice (see k_scan_tc.cu)
         const int64_t tail_tiles = (int64_t)(gridDim.x / (2 * pslices)) * CHUNK * 2;
         int csz = n_tiles > tail_tiles ? CHUNK : 1;
-        int64_t c = atomicAdd(ctr, csz);
-        int since = 0;
+        int64_t c = atomicAdd(a.ctr + cur, csz);
         for (;;) {
-          const int64_t t0 = c;
-          if (t0 >= n_tiles) break;
-          // optional lockstep window across pair slices (a.window chunks; 0 = off): keeps
-          // the pair slices' sweeps within what L2 holds (experiment knob)
-          if (a.window > 0 && pslices > 1 && ++since >= 4) {
-            since = 0;
-            for (;;) {
-              int64_t lo = n_tiles;
+          int64_t t0 = c;
+          if (t0 >= n_tiles) {
+            // Migration: this pair slice ran dry; continue the slice with the most tiles
+            // left (worth a prompt-slice reload only if it has a few chunks to go), taking
+            // one of its MAX_VISITS migrant list slots.
+            if (!a.migrate) break;
+            int next = -1;
+            for (int tries = 0; tries < 3 && next < 0; ++tries) {
+              int64_t best_rem = 8 * CHUNK - 1;
+              int cand = -1;
               for (int ps = 0; ps < pslices; ++ps) {
-                const int64_t cs = *reinterpret_cast<volatile int*>(a.ctr + ps);
-                lo = cs < lo ? cs : lo;
+                const int64_t rem = n_tiles - *reinterpret_cast<volatile int*>(a.ctr + ps);
+                if (rem > best_rem) {
+                  best_rem = rem;
+                  cand = ps;
+                }
               }
-              if (t0 <= lo + (int64_t)a.window * CHUNK) break;
-              __nanosleep(256);
+              if (cand < 0) break;
+              const int v = atomicAdd(a.ctr + 2 * MAX_SLICES + cand, 1);
+              if (v >= MAX_VISITS) continue;
+              const int64_t cc = atomicAdd(a.ctr + cand, CHUNK);
+              if (cc < n_tiles) {
+                next = cand;
+                slot = a.home_max + v;
+                c = cc;
+                csz = CHUNK;
+              }
             }
+            if (next < 0) break;
+            cur = next;
+            ++ep;
+            t0 = c;
           }
           const int64_t t1 = t0 + csz < n_tiles ? t0 + csz : n_tiles;
           csz = n_tiles - t1 > tail_tiles ? CHUNK : 1;
-          c = atomicAdd(ctr, csz);
+          c = atomicAdd(a.ctr + cur, csz);
           for (int64_t t = t0; t < t1; ++t, ++l) {
-            // ring entry l % 8 is free in both CTAs once slot 2l's previous tile (l - 4)
-            // was consumed; the wait inside issue() for hh = 0 guarantees it, so publish
-            // after that wait: do the hh = 0 wait first
+            // ring entry l % 8 is free in both CTAs once the first slot of tile l was
+            // released by its previous tile (4 or 2 tiles back): wait for that first
             const int64_t u = SPT * l;
             tc::mbar_wait(tc::smem_u32(&sm->empty[u & (NSLOT - 1)]), (uint32_t)(((u >> 3) & 1) ^ 1));
-            sm->tile_id[l & (INV_SLOTS - 1)] = t;
-            tc::st_async_s64(tc::mapa(tc::smem_u32(&sm->tile_id[l & (INV_SLOTS - 1)]), 1), t,
+            const int64_t pk = pack_tile(t, cur, slot, ep);
+            sm->tile_id[l & (INV_SLOTS - 1)] = pk;
+            tc::st_async_s64(tc::mapa(tc::smem_u32(&sm->tile_id[l & (INV_SLOTS - 1)]), 1), pk,
                              tc::mapa(tc::smem_u32(&sm->tsched[l & (INV_SLOTS - 1)]), 1));
             issue(l, t);
           }
@@ -235,13 +262,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t tb = tc::smem_u32(&sm->tsched[l & (INV_SLOTS - 1)]);
           tc::mbar_arrive_expect_tx(tb, 8);
           tc::mbar_wait(tb, (uint32_t)((l >> 3) & 1));
-          const int64_t t = *reinterpret_cast<volatile int64_t*>(&sm->tile_id[l & (INV_SLOTS - 1)]);
-          if (t < 0) {
+          const int64_t pk = *reinterpret_cast<volatile int64_t*>(&sm->tile_id[l & (INV_SLOTS - 1)]);
+          if (pk < 0) {
             tc::mbar_arrive(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]));
             ++markers;
             continue;
           }
-          issue(l, t);
+          issue(l, tile_of(pk));
         }
       }
     }
@@ -253,9 +280,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::fence_after();
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
     const uint64_t abase = tc::desc_kmajor_sw128(region_s);  // A tail (KBV = 16)
+    int my_ep = 0;
     for (int64_t l = warp == 1 ? 0 : 1;; l += 2) {
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
-      if (sm->tile_id[l & (INV_SLOTS - 1)] < 0) break;
+      const int64_t pk = sm->tile_id[l & (INV_SLOTS - 1)];
+      if (pk < 0) break;
+      if (epoch_of(pk) != my_ep) {  // both CTAs reloaded their prompt halves of the new pair slice
+        my_ep = epoch_of(pk);
+        tc::mbar_wait(tc::smem_u32(&sm->qpair), (uint32_t)(my_ep & 1));
+        tc::fence_after();
+      }
       const int b = (int)(l & 1);
       tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
       tc::fence_after();
@@ -291,7 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;
     const int h = (warp - 4) >> 2;          // column half of every tile (32 of the 64 rows)
     const int p_local = q * 32 + lane;
-    const int p = pbase + p_local;
+    const int p0 = pbase + p_local;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const uint32_t tempty_c[2] = {tc::mapa(tc::smem_u32(&sm->tempty[0]), 0), tc::mapa(tc::smem_u32(&sm->tempty[1]), 0)};
     {
@@ -320,20 +354,94 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::mbar_arrive_cluster_relaxed(tc::mapa(tc::smem_u32(&sm->qpair), 0));
       }
     }
-    const bool active = p < a.N;
-    const float iq = a.inv_q[p];
     const uint32_t scratch = region_s + (uint32_t)(REGION_BYTES + SCRATCH_OFF + (warp - 4) * 512 * 4);
+    // per-epoch state: the prompt this thread scores, its list, the shared threshold
+    int p = p0;
+    int slot = range;
+    int my_ep = 0;
+    bool active = p < a.N;
+    float iq = a.inv_q[p];
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;
     uint64_t* gthr_p = a.gthr + p;
     uint64_t published = 0;
     uint64_t gk = active ? __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p)) : 0;
+    // fold the two column halves of each prompt through the warps' slow-path scratch
+    // (half 1 parks its list in its own scratch, half 0 of the same lane quarter merges)
+    // and write one candidate list per (epoch, prompt) into list slot `slot`
+    auto flush = [&]() {
+      const uint32_t mine = scratch + (uint32_t)(lane * KMAX * 8);
+      const uint32_t partner = mine + (uint32_t)(4 * 512 * 4);  // warp q + 8's scratch, same lane
+      if (h == 1) {
+#pragma unroll
+        for (int t2 = 0; t2 < KMAX; ++t2) tc::sts_u64(mine + t2 * 8, tl.v[t2]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+      if (h == 0 && active) {
+#pragma unroll
+        for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(tc::lds_u64(partner + t2 * 8));
+        uint64_t* out = a.partial + ((int64_t)slot * a.N + p) * a.k;
+#pragma unroll
+        for (int t2 = 0; t2 < KMAX; ++t2)
+          if (t2 < a.k) out[t2] = tl.v[t2];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");  // scratch free again
+    };
     for (int64_t l = 0;; ++l) {
       __syncwarp();
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
-      const int64_t t = sm->tile_id[l & (INV_SLOTS - 1)];
-      if (t < 0) break;
+      const int64_t pk = sm->tile_id[l & (INV_SLOTS - 1)];
+      if (pk < 0) break;
+      if (epoch_of(pk) != my_ep) {
+        // Migration: every tile of the previous epoch is done (tiles are processed in
+        // order and each one's accumulator was read after its MMAs, which read both
+        // CTAs' A), so the old list is final and the A operand may be replaced by this
+        // CTA's half of the new pair slice, loaded straight from global memory.
+        flush();
+        my_ep = epoch_of(pk);
+        slot = slot_of(pk);
+        p = pslice_of(pk) * 2 * TM + (int)crank * TM + p_local;
+        const uint4* src = reinterpret_cast<const uint4*>(a.Xb + (int64_t)p * a.d);
+        const int KBT = KB < KB_TMEM ? KB : KB_TMEM;
+        for (int c = h; c < KBT; c += 2) {
+          uint32_t r[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 u4 = __ldcg(src + c * 8 + j);
+            r[4 * j + 0] = u4.x;
+            r[4 * j + 1] = u4.y;
+            r[4 * j + 2] = u4.z;
+            r[4 * j + 3] = u4.w;
+          }
+          tc::tmem_st32(tmem + lane_base + (uint32_t)(c * 32), r);
+        }
+        if (KBV > KB_TMEM) {  // the A tail in shared memory, in the TMA's 128-byte swizzle
+          const int sw = p_local & 7;
+          for (int c = KB_TMEM + h; c < KB; c += 2)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 u4 = __ldcg(src + c * 8 + j);
+              const uint32_t dst = region_s + (uint32_t)((c - KB_TMEM) * QBOX_BYTES + p_local * 128 + ((j ^ sw) << 4));
+              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(u4.x), "r"(u4.y), "r"(u4.z),
+                           "r"(u4.w)
+                           : "memory");
+            }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        tc::tmem_wait_st();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&sm->qpair), 0));  // release: smem A tail
+        active = p < a.N;
+        iq = a.inv_q[p];
+        tl.clear();
+        thr = active ? -INFINITY : INFINITY;
+        gthr_p = a.gthr + p;
+        published = 0;
+        gk = active ? __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p)) : 0;
+      }
+      const int64_t t = tile_of(pk);
       if (gk != 0) thr = fmaxf(thr, key_score(gk));
       const int b = (int)(l & 1);
       const int64_t j0 = t * TN + h * 32;
@@ -358,22 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (active && (l & 3) == 3) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
       }
     }
-    // fold the two column halves of each prompt (the ring is idle: all MMAs of this
-    // pair completed before the last accumulator was read)
-    const uint32_t xchg = ring_s + (uint32_t)((q * 32 + lane) * KMAX * 8);
-    if (h == 1) {
-#pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2) tc::sts_u64(xchg + t2 * 8, tl.v[t2]);
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
-    if (h == 0 && active) {
-#pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(tc::lds_u64(xchg + t2 * 8));
-      uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
-#pragma unroll
-      for (int t2 = 0; t2 < KMAX; ++t2)
-        if (t2 < a.k) out[t2] = tl.v[t2];
-    }
+    flush();
   }
 
   tc::fence_before();
@@ -442,7 +535,7 @@ cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, con
                              cudaStream_t s, bool pdl) {
   const int pslices = (a.N + 2 * TM - 1) / (2 * TM);
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
-  const dim3 grid(2 * pslices * a.P);
+  const dim3 grid(a.migrate ? a.grid_ctas : 2 * pslices * a.P);
   // several 128-prompt slices re-read each tile: normal L2 policy (ARGUS_SCAN_L2 overrides)
   static int l2env = -2;
   if (l2env == -2) {

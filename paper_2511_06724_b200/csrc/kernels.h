@@ -44,11 +44,17 @@ struct ScanArgs {
   uint64_t* partial;         // [P][N][k] per-CTA-range candidates
   int32_t P;                 // number of cache ranges (filled by the planner)
   uint64_t* gthr;            // [n_pad] per-prompt shared top-k threshold key (zeroed by K6)
-  int32_t* ctr;              // [MAX_SLICES] per-slice tile-chunk work counters (zeroed by K6)
+  int32_t* ctr;              // [CTR_WORDS] (zeroed by K6): per-slice tile counters [0, MAX_SLICES),
+                             // pair-slice visit counters [2 MAX_SLICES, 3 MAX_SLICES) (migration)
   uint32_t head, capg;       // ring eviction: oldest live cache position, capacity (0, 0 when not wrapped)
   int32_t window;            // pair scan: max chunks a pair slice may lead the slowest (0 = off)
+  int32_t migrate;           // pair scan: pairs whose slice runs dry continue another slice
+  int32_t home_max;          // pair scan: list slots [0, home_max) belong to home pairs
+  int32_t grid_ctas;         // pair scan with migration: CTAs launched (all SMs' pairs)
 };
 constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts
+constexpr int CTR_WORDS = 3 * MAX_SLICES;
+constexpr int MAX_VISITS = 4;   // migrant pairs per pair slice (list slots home_max .. home_max + 3)
 
 // K0: fp32 rows -> bf16 stripe + inverse norms; rows g in [g0, g0+n) whose
 // g % world == rank go to slot g / world.

@@ -361,3 +361,21 @@ def test_async_host_calls_match_sync(argus_mod, pipeline):
         for key in ("option", "topk_idx", "topk_score", "quality", "status"):
             np.testing.assert_array_equal(o[key], rf[1][key])
     assert rcs[3] == 1   # ARGUS_W_OVERFLOW
+
+
+@pytest.mark.parametrize("N,M,seed", [(768, 90000, 151), (1300, 80000, 152)])
+def test_pair_scan_migration(argus_mod, N, M, seed):
+    """More pair slices than divide the 74 TPC pairs evenly (N = 768: 3 pair slices;
+    N = 1300: 6): every TPC runs a pair, pairs whose slice runs dry reload another
+    slice's prompts and continue its tiles.  Top-k and assignment must be exact."""
+    p = gen.small_problem("C2", N=N, M=M, seed=seed)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    with make_router(argus_mod, p) as r:
+        r.argus_cache_insert(p.cache)
+        rc, g = r.argus_route_batch(p.X, quota)
+        rc2, g2 = r.argus_route_batch(p.X, quota)
+    np.testing.assert_array_equal(g["topk_idx"], g2["topk_idx"])    # migration timing never changes results
+    rows = list(range(0, N, 3))
+    parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"], rows=rows)
+    parity.check_replay(g, p.opts, quota)
+    parity.invariants(g, p.opts, quota)

@@ -534,7 +534,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   // lists per prompt x prompts: <= num_sms * 128 for the one-slice-per-CTA scan; the
   // pair scan with migration adds MAX_VISITS slots per pair slice
   // (home_max + MAX_VISITS) * N <= (num_sms / 2 / pslices + 1 + MAX_VISITS) * 256 * pslices
-  r->partial_lists = (int64_t)r->num_sms * 128 + (int64_t)(MAX_VISITS + 1) * (((int64_t)c.max_batch + 255) / 256 * 256);
+  // pair scan with migration: P = home + floaters + MAX_VISITS <= num_sms / 2 / pslices +
+  // pslices + MAX_VISITS, times N <= 256 * pslices
+  r->partial_lists = (int64_t)r->num_sms * 128 + (int64_t)(MAX_VISITS + 1 + MAX_SLICES / 2) *
+                                                     (((int64_t)c.max_batch + 255) / 256 * 256);
   for (int q = 0; q < 2; ++q) {
     TRY_RC(dalloc(r, &r->d_Xb[q], (size_t)r->n_pad_max * d));
     TRY_RC(dalloc(r, &r->d_partial[q], (size_t)r->partial_lists * k));
@@ -880,14 +883,16 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
       const int64_t n_tiles = (a.m_local + 63) / 64;
       a.migrate = r->migrate && pslices >= 2 && clusters % pslices != 0 && n_tiles >= (int64_t)clusters * 16;
       if (a.migrate) {
-        a.home_max = (clusters + pslices - 1) / pslices;
-        a.P = a.home_max + MAX_VISITS;
+        a.home_max = clusters / pslices;
+        a.floaters = clusters - a.home_max * pslices;
+        a.P = a.home_max + a.floaters + MAX_VISITS;
         a.grid_ctas = 2 * clusters;
         if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
         CU_TRY(r, cudaMemsetAsync(r->d_partial[q], 0, sizeof(uint64_t) * (size_t)a.P * N * k, s_scan));
       } else {
         a.P = scan_pair_plan(a.m_local, N, r->num_sms);
         a.home_max = a.P;
+        a.floaters = 0;
       }
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
       if (launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined) != cudaSuccess) {

@@ -108,8 +108,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t crank = tc::cluster_ctarank();  // 0 = leader (issues the MMAs)
   const bool leader = crank == 0;
   const int pair = blockIdx.x >> 1;
-  const int pslice = pair % pslices;
-  const int range = pair / pslices;               // candidate list index of this pair's CTAs
+  // With migration the first home_max * pslices pairs are homed round-robin on the pair
+  // slices and the rest "float": they keep moving to the slice that is furthest behind,
+  // so all slices sweep the cache at about the same pace (L2 reuse) on every TPC.
+  const int n_home = a.migrate ? a.home_max * pslices : 1 << 30;
+  const bool floater = pair >= n_home;
+  const int pslice = floater ? (pair - n_home) % pslices : pair % pslices;
+  const int range = floater ? a.home_max + (pair - n_home) : pair / pslices;  // this pair's list slot
   const int KB = a.d / KBLK;
   const int pbase = pslice * 2 * TM + (int)crank * TM;  // this CTA's first prompt
 
@@ -188,19 +193,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (leader) {
         // A tile entry carries the tile, the pair slice, the list slot and the epoch
         // (pack_tile); consumers reload the prompt slice when the epoch changes.
-        int cur = pslice, slot = range, ep = 0;
+        int cur = pslice, slot = range, ep = 0, since = 0;
         int64_t l = 0;
         // tile-granular counter: CHUNK tiles per grab, single tiles for the last two
         // chunks per pair of the pair slice (see k_scan_tc.cu)
         const int64_t tail_tiles = (int64_t)(gridDim.x / (2 * pslices)) * CHUNK * 2;
+        // the pair slice furthest behind that still has some chunks to go (or `keep`)
+        auto laggard = [&](int keep) {
+          int64_t lo = *reinterpret_cast<volatile int*>(a.ctr + keep);
+          int best = keep;
+          for (int ps = 0; ps < pslices; ++ps) {
+            const int64_t cs = *reinterpret_cast<volatile int*>(a.ctr + ps);
+            if (cs + 8 * CHUNK < n_tiles && cs < lo) {
+              lo = cs;
+              best = ps;
+            }
+          }
+          return best;
+        };
         int csz = n_tiles > tail_tiles ? CHUNK : 1;
         int64_t c = atomicAdd(a.ctr + cur, csz);
+        int c_ps = cur;  // the pair slice `c` was taken from
         for (;;) {
           int64_t t0 = c;
+          if (c_ps != cur) {  // a floater's move takes effect with the chunk it prefetched
+            cur = c_ps;
+            ++ep;
+          }
           if (t0 >= n_tiles) {
             // Migration: this pair slice ran dry; continue the slice with the most tiles
-            // left (worth a prompt-slice reload only if it has a few chunks to go), taking
-            // one of its MAX_VISITS migrant list slots.
+            // left (worth a prompt-slice reload only if it has a few chunks to go).  Home
+            // pairs take one of its MAX_VISITS migrant list slots; floaters keep theirs.
             if (!a.migrate) break;
             int next = -1;
             for (int tries = 0; tries < 3 && next < 0; ++tries) {
@@ -214,24 +237,35 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
               }
               if (cand < 0) break;
-              const int v = atomicAdd(a.ctr + 2 * MAX_SLICES + cand, 1);
-              if (v >= MAX_VISITS) continue;
+              int v = 0;
+              if (!floater) {
+                v = atomicAdd(a.ctr + 2 * MAX_SLICES + cand, 1);
+                if (v >= MAX_VISITS) continue;
+              }
               const int64_t cc = atomicAdd(a.ctr + cand, CHUNK);
               if (cc < n_tiles) {
                 next = cand;
-                slot = a.home_max + v;
+                if (!floater) slot = a.home_max + a.floaters + v;
                 c = cc;
                 csz = CHUNK;
               }
             }
             if (next < 0) break;
-            cur = next;
+            cur = c_ps = next;
             ++ep;
             t0 = c;
           }
           const int64_t t1 = t0 + csz < n_tiles ? t0 + csz : n_tiles;
           csz = n_tiles - t1 > tail_tiles ? CHUNK : 1;
-          c = atomicAdd(a.ctr + cur, csz);
+          // next grab: a floater re-balances every 8 chunks
+          int nps = cur;
+          if (floater && ++since >= 8) {
+            since = 0;
+            nps = laggard(cur);
+            if (nps != cur) csz = CHUNK;
+          }
+          c = atomicAdd(a.ctr + nps, csz);
+          c_ps = nps;
           for (int64_t t = t0; t < t1; ++t, ++l) {
             // ring entry l % 8 is free in both CTAs once the first slot of tile l was
             // released by its previous tile (4 or 2 tiles back): wait for that first
@@ -382,6 +416,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(tc::lds_u64(partner + t2 * 8));
         uint64_t* out = a.partial + ((int64_t)slot * a.N + p) * a.k;
+        if (a.migrate)  // a floater's slot may already hold its list from an earlier visit
+#pragma unroll
+          for (int t2 = 0; t2 < KMAX; ++t2)
+            if (t2 < a.k) tl.insert(out[t2]);
 #pragma unroll
         for (int t2 = 0; t2 < KMAX; ++t2)
           if (t2 < a.k) out[t2] = tl.v[t2];

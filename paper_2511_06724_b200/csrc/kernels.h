@@ -49,7 +49,8 @@ struct ScanArgs {
   uint32_t head, capg;       // ring eviction: oldest live cache position, capacity (0, 0 when not wrapped)
   int32_t window;            // pair scan: max chunks a pair slice may lead the slowest (0 = off)
   int32_t migrate;           // pair scan: pairs whose slice runs dry continue another slice
-  int32_t home_max;          // pair scan: list slots [0, home_max) belong to home pairs
+  int32_t home_max;          // pair scan: home pairs per pair slice = their list slots [0, home_max)
+  int32_t floaters;          // pair scan: pairs beyond home_max * pair slices (slots home_max + f)
   int32_t grid_ctas;         // pair scan with migration: CTAs launched (all SMs' pairs)
 };
 constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts

@@ -184,8 +184,11 @@ int argus_route_batch_dev(argus_router* r, const float* prompts_dev, int32_t N,
  * outputs back into the caller's host buffers (same meaning as argus_route_batch;
  * quality_out / status_out may be NULL), then returns at once with *ticket set to
  * an increasing call id.  All buffers must stay alive and untouched until
- * argus_route_wait(r, *ticket) returns; use pinned (page-locked) host memory, or the
- * copies run synchronously.  With cfg.pipeline = 1 consecutive calls overlap (the
+ * argus_route_wait(r, *ticket) returns; the prompts should be pinned (page-locked)
+ * host memory, or their copy runs synchronously.  The outputs travel back in one
+ * packed copy into the library's pinned staging and are unpacked into the caller's
+ * buffers when the call is collected (argus_route_wait / argus_sync, or when its
+ * staging slot is reused four calls later).  With cfg.pipeline = 1 consecutive calls overlap (the
  * tail of one with the scan of the next).  A call waits (on the host) for the call
  * issued four calls before it to finish.  Returns ARGUS_OK once enqueued or an
  * argument error; the call's own result comes from argus_route_wait. */

@@ -147,6 +147,17 @@ struct argus_router {
   uint8_t* d_oasync[NASYNC] = {};
   uint32_t* h_fasync = nullptr;    // [NASYNC] pinned flag words
   cudaEvent_t ev_async[NASYNC] = {};
+  uint8_t* h_oasync[NASYNC] = {};      // pinned staging of each slot's packed outputs
+  cudaStream_t d2h_stream = nullptr;   // result copies (off the tail stream)
+  cudaEvent_t ev_done[NASYNC] = {};    // the slot's tail finished
+  struct AsyncOut {                    // where harvest copies a slot's results
+    int32_t N = 0;
+    int32_t* option = nullptr;
+    uint32_t* idx = nullptr;
+    float* score = nullptr;
+    float* quality = nullptr;
+    uint8_t* status = nullptr;
+  } aout[NASYNC];
   int64_t async_ticket[NASYNC] = {-1, -1, -1, -1};  // ticket whose D2H the slot carries (-1: none)
   int64_t next_ticket = 0;
   std::map<int64_t, int> async_rc;     // harvested results of finished tickets
@@ -416,8 +427,14 @@ int argus_route_destroy(argus_router* r) {
   if (r->h_flags) cudaFreeHost(r->h_flags);
   if (r->h_outblk) cudaFreeHost(r->h_outblk);
   if (r->h_fasync) cudaFreeHost(r->h_fasync);
+  if (r->d2h_stream) cudaStreamSynchronize(r->d2h_stream);
   for (cudaEvent_t e : r->ev_async)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : r->ev_done)
+    if (e) cudaEventDestroy(e);
+  for (uint8_t* h : r->h_oasync)
+    if (h) cudaFreeHost(h);
+  if (r->d2h_stream) cudaStreamDestroy(r->d2h_stream);
   if (r->d_outblk) cudaFree(r->d_outblk);
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
@@ -570,7 +587,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   for (int q = 0; q < argus_router::NASYNC; ++q) {
     TRY_RC(dalloc(r, &r->d_Xasync[q], (size_t)c.max_batch * d));
     TRY_RC(dalloc(r, &r->d_oasync[q], 16 + 16 * 8 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1)));
-    if (cudaEventCreateWithFlags(&r->ev_async[q], cudaEventDisableTiming) != cudaSuccess) {
+    if (cudaMallocHost((void**)&r->h_oasync[q], 16 + 16 * 8 + (size_t)c.max_batch * (4 + 8 * (size_t)k + 4 * (size_t)L + 1)) !=
+            cudaSuccess ||
+        cudaEventCreateWithFlags(&r->ev_done[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&r->ev_async[q], cudaEventDisableTiming) != cudaSuccess) {
       argus_route_destroy(r);
       return ARGUS_E_CUDA;
     }
@@ -581,6 +601,10 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     return ARGUS_E_CUDA;
   }
   for (int q = 0; q <= argus_router::NASYNC; ++q) r->h_fasync[q] = 0u;
+  if (cudaStreamCreateWithFlags(&r->d2h_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    argus_route_destroy(r);
+    return ARGUS_E_CUDA;
+  }
   TRY_RC(dalloc(r, &r->d_worker, (size_t)c.max_batch));
   r->outblk_bytes = 16 + 16 * 8 + (size_t)c.max_batch * (4 + 16 * (size_t)k + 4 * (size_t)L + 1 + 8);
   TRY_RC(dalloc(r, &r->d_outblk, r->outblk_bytes));
@@ -1193,7 +1217,23 @@ static int flags_rc(uint32_t fl) {
 static int async_harvest(argus_router* r, int q) {
   if (r->async_ticket[q] < 0) return ARGUS_OK;
   CU_TRY(r, cudaEventSynchronize(r->ev_async[q]));
-  r->async_rc[r->async_ticket[q]] = flags_rc(r->h_fasync[q]);
+  // one packed copy landed in pinned staging: unpack into the caller's buffers
+  const argus_router::AsyncOut& o = r->aout[q];
+  const int N = o.N, k = r->cfg.k, L = r->cfg.L;
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_opt = 16, o_idx = al(o_opt + 4 * (size_t)N), o_sc = al(o_idx + 4 * (size_t)N * k),
+               o_rh = al(o_sc + 4 * (size_t)N * k), o_st = al(o_rh + 4 * (size_t)N * L);
+  const uint8_t* Hb = r->h_oasync[q];
+  memcpy(o.option, Hb + o_opt, 4 * (size_t)N);
+  if (k > 0) {
+    memcpy(o.idx, Hb + o_idx, 4 * (size_t)N * k);
+    memcpy(o.score, Hb + o_sc, 4 * (size_t)N * k);
+  }
+  if (o.quality) memcpy(o.quality, Hb + o_rh, 4 * (size_t)N * L);
+  if (o.status) memcpy(o.status, Hb + o_st, (size_t)N);
+  uint32_t fl;
+  memcpy(&fl, Hb, 4);
+  r->async_rc[r->async_ticket[q]] = flags_rc(fl);
   r->async_ticket[q] = -1;
   return ARGUS_OK;
 }
@@ -1230,17 +1270,15 @@ int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, co
                                 quality_out ? reinterpret_cast<float*>(D + o_rh) : nullptr, D + o_st, nullptr);
   r->flags_cur = nullptr;
   if (rc) return rc;
-  // results back to the caller's buffers, ordered after this call's tail
+  // results: one packed device-to-host copy on the copy stream once this call's tail
+  // is done (the tail stream itself is never held up by copies); harvest unpacks it
   cudaStream_t s = (r->pipe && r->tail_inflight[(r->seq - 1) & 1]) ? r->tail_stream : r->stream;
-  CU_TRY(r, cudaMemcpyAsync(option_out, D + o_opt, 4 * (size_t)N, cudaMemcpyDeviceToHost, s));
-  if (k > 0) {
-    CU_TRY(r, cudaMemcpyAsync(topk_idx, D + o_idx, 4 * (size_t)N * k, cudaMemcpyDeviceToHost, s));
-    CU_TRY(r, cudaMemcpyAsync(topk_score, D + o_sc, 4 * (size_t)N * k, cudaMemcpyDeviceToHost, s));
-  }
-  if (quality_out) CU_TRY(r, cudaMemcpyAsync(quality_out, D + o_rh, 4 * (size_t)N * L, cudaMemcpyDeviceToHost, s));
-  if (status_out) CU_TRY(r, cudaMemcpyAsync(status_out, D + o_st, (size_t)N, cudaMemcpyDeviceToHost, s));
-  CU_TRY(r, cudaMemcpyAsync(r->h_fasync + q, dflags, 4, cudaMemcpyDeviceToHost, s));
-  CU_TRY(r, cudaEventRecord(r->ev_async[q], s));
+  CU_TRY(r, cudaEventRecord(r->ev_done[q], s));
+  CU_TRY(r, cudaStreamWaitEvent(r->d2h_stream, r->ev_done[q], 0));
+  const size_t o_end = o_st + (size_t)N;
+  CU_TRY(r, cudaMemcpyAsync(r->h_oasync[q], D, o_end, cudaMemcpyDeviceToHost, r->d2h_stream));
+  CU_TRY(r, cudaEventRecord(r->ev_async[q], r->d2h_stream));
+  r->aout[q] = {N, option_out, topk_idx, topk_score, quality_out, status_out};
   r->async_ticket[q] = r->next_ticket;
   *ticket = r->next_ticket++;
   return ARGUS_OK;

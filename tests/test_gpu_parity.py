@@ -363,12 +363,12 @@ def test_async_host_calls_match_sync(argus_mod, pipeline):
     assert rcs[3] == 1   # ARGUS_W_OVERFLOW
 
 
-@pytest.mark.parametrize("N,M,seed", [(768, 90000, 151), (1300, 80000, 152)])
-def test_pair_scan_migration(argus_mod, N, M, seed):
+@pytest.mark.parametrize("N,M,k,seed", [(768, 90000, 4, 151), (1300, 80000, 4, 152), (768, 85000, 8, 153)])
+def test_pair_scan_migration(argus_mod, N, M, k, seed):
     """More pair slices than divide the 74 TPC pairs evenly (N = 768: 3 pair slices;
     N = 1300: 6): every TPC runs a pair, pairs whose slice runs dry reload another
     slice's prompts and continue its tiles.  Top-k and assignment must be exact."""
-    p = gen.small_problem("C2", N=N, M=M, seed=seed)
+    p = gen.small_problem("C2", N=N, M=M, k=k, seed=seed)
     quota = oracle.quota_from_fractions(p.fractions, N)
     with make_router(argus_mod, p) as r:
         r.argus_cache_insert(p.cache)

@@ -5,6 +5,10 @@
 #include <cstdint>
 #include <cuda.h>
 
+#ifndef ARGUS_MBAR_SUSPEND_NS
+#define ARGUS_MBAR_SUSPEND_NS 0  // > 0: mbarrier waits carry this suspend-time hint (ns)
+#endif
+
 namespace argus {
 namespace tc {
 
@@ -38,8 +42,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp may be parked by the hardware
+// until the phase completes (or the hint expires) instead of spinning, which frees
+// issue slots and power for the warps doing work
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(ARGUS_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  if (ARGUS_MBAR_SUSPEND_NS > 0) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
+    }
+  } else {
+    while (!mbar_try_wait(bar, parity)) {
+    }
   }
 }
 

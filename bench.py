@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of fixed N: per-N stage times to stderr")
     ap.add_argument("--fixed-n", type=int, default=0, help="diagnostics: every batch has this N")
+    ap.add_argument("--force-nccl", action="store_true",
+                    help="diagnostics: on one GPU, run the multi-GPU data path through a one-rank NCCL communicator")
     ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
                     help="1: the tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline)")
     return ap.parse_args()
@@ -193,10 +195,12 @@ def main():
 
     from paper_2511_06724_b200 import dist as adist
     uid = adist.share_nccl_id(dist, rank, argus.argus_nccl_unique_id) if world > 1 else None
+    if world == 1 and args.force_nccl:
+        uid = argus.argus_nccl_unique_id()
     stream = torch.cuda.Stream()
     r = argus.Router(d, k, opts, W1, b1, W2, b2, capacity=cfg.M, max_batch=max_batch, rank=rank, world=world,
                      device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream,
-                     pipeline=bool(args.pipeline) and world == 1)
+                     pipeline=bool(args.pipeline) and world == 1 and uid is None)
 
     # ---- cache: generated chunk by chunk, inserted through the ABI (rank 0 authoritative)
     cg = gen.CacheGen(cfg.M, d, cfg.seed)

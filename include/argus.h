@@ -101,7 +101,10 @@ typedef struct {
  *   delta      optimal-quality threshold (0.9); compared as float r >= delta
  *   rank, world, device   this process's rank, world size (1 = single GPU), CUDA device
  *   nccl_unique_id        128-byte ncclUniqueId identical on all ranks, or NULL
- *                         (world == 1, or external collective mode)
+ *                         (single GPU, or external collective mode).  With
+ *                         world == 1 a unique id builds a one-rank communicator:
+ *                         the multi-GPU data path (broadcasts, all-gather,
+ *                         per-shard merge) on one GPU, for testing
  *   stream     cudaStream_t to run on, or NULL (the library creates one)
  *   evict      0: an insert past capacity fails (ARGUS_E_CAPACITY).  1: ring
  *              eviction of the oldest entries (capacity % world == 0); see

@@ -229,7 +229,9 @@ static int dalloc(argus_router* r, T** p, size_t n) {
   return ARGUS_OK;
 }
 
-static bool nccl_mode(const argus_router* r) { return r->cfg.world > 1 && r->comm != nullptr; }
+// NCCL collectives in the data path: world > 1 with a unique id, or world == 1 with a
+// unique id (a one-rank communicator: the multi-GPU code path on one GPU, for tests)
+static bool nccl_mode(const argus_router* r) { return r->comm != nullptr; }
 
 // transpose / round the predictor weights on the device (init time)
 __global__ void k_prep_weights(const float* __restrict__ w1, int d, int k, int H, float* __restrict__ W1sT) {
@@ -501,7 +503,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) { delete r; return ARGUS_E_CUDA; }
     r->own_stream = true;
   }
-  r->pipe = c.pipeline != 0 && c.world == 1;
+  r->pipe = c.pipeline != 0 && c.world == 1 && c.nccl_unique_id == nullptr;
   r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
   r->migrate = getenv("ARGUS_NO_MIGRATE") == nullptr;
@@ -518,7 +520,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
            cudaEventCreateWithFlags(&r->ev_tail[q], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) { argus_route_destroy(r); return ARGUS_E_CUDA; }
   }
-  if (c.world > 1 && c.nccl_unique_id) {
+  if (c.nccl_unique_id) {
     ncclUniqueId id;
     memcpy(&id, c.nccl_unique_id, sizeof(id));
     if (!nccl().ok || nccl().CommInitRank(&r->comm, c.world, id, c.rank) != ncclSuccess) {

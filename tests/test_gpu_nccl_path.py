@@ -1,0 +1,51 @@
+"""The multi-GPU data path on one GPU: a router built with world = 1 and an NCCL
+unique id runs every collective of the G-GPU path through a one-rank NCCL
+communicator (rank 0's rows and prompts broadcast, the per-shard K5 merge, the
+all-gather of the N x k candidate keys, the handle broadcast) and must return
+exactly what the single-GPU router returns."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import argus_inputs as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def argus_mod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2511_06724_b200 import argus
+    return argus
+
+
+@pytest.mark.parametrize("N,M,evict", [(300, 20000, False), (200, 9000, True), (77, 4133, False)])
+def test_one_rank_nccl_path_matches_single_gpu(argus_mod, N, M, evict):
+    import torch
+    argus = argus_mod
+    p = gen.small_problem("C2", N=N, M=M, seed=171)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    cap = M - M // 3 if evict else M + 64
+    handles = np.arange(M, dtype=np.uint64) * np.uint64(3) + np.uint64(5)
+    outs = []
+    for uid in (None, argus.argus_nccl_unique_id()):
+        with argus.Router(768, p.k, p.opts, p.W1, p.b1, p.W2, p.b2, capacity=cap, max_batch=N, evict=evict,
+                          nccl_unique_id=uid) as r:
+            r.argus_cache_insert_h(p.cache[: M // 2], handles[: M // 2])
+            r.argus_cache_insert_h(p.cache[M // 2:], handles[M // 2:])
+            rc, g = r.argus_route_batch_ex(p.X, quota, want_handles=True)
+            X = torch.from_numpy(p.X).cuda()
+            o = dict(option=torch.empty(N, dtype=torch.int32, device="cuda"),
+                     topk_idx=torch.empty((N, p.k), dtype=torch.int32, device="cuda"),
+                     topk_score=torch.empty((N, p.k), dtype=torch.float32, device="cuda"))
+            r.argus_route_batch_dev(X, quota, o["option"], o["topk_idx"], o["topk_score"])
+            r.argus_sync()
+            g["dev_option"] = o["option"].cpu().numpy()
+            g["dev_idx"] = o["topk_idx"].cpu().numpy().view(np.uint32)
+            outs.append((rc, g))
+    (rc0, a), (rc1, b) = outs
+    assert rc0 == rc1
+    for key in ("option", "topk_idx", "topk_score", "quality", "status", "optimal", "topk_handle", "dev_option",
+                "dev_idx"):
+        np.testing.assert_array_equal(a[key], b[key], err_msg=key)

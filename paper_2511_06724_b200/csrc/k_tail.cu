@@ -476,13 +476,19 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     // lane v owns option v: z_v = b2_v + sum_j W2[v][j] h_j, four interleaved partial
     // sums in a compact (not unrolled) loop -- this phase runs once per CTA from a cold
     // instruction cache, so code size, not arithmetic, is what costs here
+    // With L <= 16 lanes v and v + 16 each take half of the hidden units of option v
+    // and add their halves with one shuffle (fadd is commutative: both lanes get the
+    // same bits), halving the loop on the tail's critical path.
     float z = 0.f;
-    if (act) {
+    const bool split = L <= 16;
+    const int ov = split ? (lane & 15) : lane;
+    if (ov < L) {
       float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      const float* w2r = w2s + lane * H4;
+      const float* w2r = w2s + ov * H4;
       const float* hp = hs + p * H;
+      const int jb = split ? (lane >> 4) * (H / 2) : 0, je = split ? jb + H / 2 : H;
 #pragma unroll 1
-      for (int j = 0; j < H; j += 4) {
+      for (int j = jb; j < je; j += 4) {
         const float4 w4 = *reinterpret_cast<const float4*>(w2r + j);
         const float4 h4 = *reinterpret_cast<const float4*>(hp + j);
         z0 = __fmaf_rn(w4.x, h4.x, z0);
@@ -492,6 +498,7 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       }
       z = __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));
     }
+    if (split) z = __fadd_rn(z, __shfl_xor_sync(0xffffffffu, z, 16));
     float rr = 0.f;
     if (act) {
       z = __fadd_rn(z, a.b2[lane]);

@@ -247,3 +247,12 @@ def test_allocation_matches_lp_relaxation_bound():
             res = linprog(-np.array(Q), A_eq=[np.ones(Lv)], b_eq=[W], bounds=[(0, c) for c in caps], method="highs")
             best = max(best, -res.fun / W)
         assert abs(best - r["objective"]) < 1e-9
+
+
+def test_affinity_histogram_window():
+    """H(v) over the last 1000 prompts' optimal options (hand-countable)."""
+    hist = [0] * 700 + [3] * 500 + [1] * 300
+    h = oc.affinity_histogram(hist, 4)
+    assert list(h) == [200, 300, 0, 500]          # the first 500 zeros fell out of the window
+    assert list(oc.affinity_histogram([2, 2, 1], 4)) == [0, 1, 2, 0]
+    assert list(oc.affinity_histogram(hist, 4, window=10)) == [0, 10, 0, 0]

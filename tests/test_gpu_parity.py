@@ -379,3 +379,25 @@ def test_pair_scan_migration(argus_mod, N, M, k, seed):
     parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"], rows=rows)
     parity.check_replay(g, p.opts, quota)
     parity.invariants(g, p.opts, quota)
+
+
+def test_largest_shapes(argus_mod):
+    """The ABI's largest shapes at once: max_batch 8192, d = 1024, k = 8, L = 32
+    (4 models x 8 skip levels) -- the CTA-pair scan with floating pairs, 8-key
+    lists, a 32-lane option table in the tail."""
+    N, M, d, k = 8192, 50000, 1024, 8
+    p = gen.small_problem("C4", N=N, M=M, d=d, k=k, seed=181)
+    opts = gen.option_table(("SD-XL", "SD-2.1", "SD-Small", "Tiny-SD"), (0, 3, 6, 9, 12, 15, 18, 21))
+    assert len(opts) == 32
+    W1, b1, W2, b2 = gen.mlp_weights(d, k, 256, 32)
+    quota = oracle.quota_from_fractions(gen.load_fractions(32, 1.1), N)
+    with argus_mod.Router(d, k, opts, W1, b1, W2, b2, capacity=M, max_batch=N) as r:
+        r.argus_cache_insert(p.cache)
+        rc, g = r.argus_route_batch(p.X, quota)
+    rows = list(range(0, N, 128)) + [N - 1]
+    parity.check_topk(p.X, p.cache, k, g["topk_idx"], g["topk_score"], rows=rows)
+    err = float(np.abs(oracle.mlp(p.X, g["topk_score"].astype(np.float64), W1, b1, W2, b2) - g["quality"]).max())
+    assert err <= parity.SCORE_TOL
+    rep = parity.check_replay(g, opts, quota)
+    assert rc == rep["rc"]
+    parity.invariants(g, opts, quota)

@@ -36,7 +36,10 @@
  * id g lives on rank g mod world at local slot g div world.  argus_cache_insert
  * and argus_route_batch* are collectives (every rank calls them in the same
  * order).  With an NCCL unique id, rank 0's inputs are authoritative (other
- * ranks may pass NULL inputs) and are broadcast by the library; the per-shard
+ * ranks may pass NULL inputs) and are broadcast by the library -- the rows, the
+ * prompts and, for argus_route_batch* under ARGUS_POLICY_SD, the quotas (a
+ * negative rank-0 quota then fails the call on every rank with ARGUS_E_INVALID,
+ * reported like an invalid prompt); the per-shard
  * top-k candidates are exchanged with one all-gather of N*k u64 keys.  Without
  * a unique id ("external" mode) every rank passes the same inputs and the
  * caller moves the keys between argus_route_partial_dev and

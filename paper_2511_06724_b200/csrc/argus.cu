@@ -138,7 +138,8 @@ struct argus_router {
   uint8_t* h_outblk = nullptr;     // pinned mirror
   size_t outblk_bytes = 0;
   bool pending = false;            // async (_dev) work enqueued since the last argus_sync
-  bool serial_call = false;        // host-buffer call in progress: one stream with PDL, no event hops
+  bool serial_call = false;
+  bool quota_dev_next = false;     // the next tail reads d_quota (set by the broadcast path)        // host-buffer call in progress: one stream with PDL, no event hops
   // asynchronous host-buffer calls (argus_route_batch_async): per-parity device
   // staging of the prompts and outputs, per-parity flags, completion events
   uint32_t* flags_cur = nullptr;   // flags word the kernels of the current call OR into
@@ -172,6 +173,7 @@ struct argus_router {
   int32_t n_workers = 0;
   int16_t* d_wlist = nullptr;      // [32][32]
   int32_t* d_wcount = nullptr;     // [32]
+  int32_t* d_quota = nullptr;      // [32] quotas broadcast from rank 0 (NCCL mode, route_batch*)
   float* d_wtime = nullptr;        // [MAX_WORKERS]
   int32_t* d_queue = nullptr;      // [MAX_WORKERS]
   uint64_t* d_handle = nullptr;    // [capacity] latent handles by cache position (replicated on every rank)
@@ -582,6 +584,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_aff, ARGUS_AFFINITY_WINDOW));
   TRY_RC(dalloc(r, &r->d_wlist, 32 * 32));
   TRY_RC(dalloc(r, &r->d_wcount, 32));
+  TRY_RC(dalloc(r, &r->d_quota, 32));
   TRY_RC(dalloc(r, &r->d_wtime, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_queue, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_optimal, (size_t)c.max_batch));
@@ -822,8 +825,11 @@ static int64_t ring_head(const argus_router* r) {
 // K6 + scan (+ K5 local merge into keys_dev when keys_dev != NULL).  *P_out receives
 // the number of per-range candidate lists left in d_partial.
 // q selects the double-buffered per-batch buffers (bf16 prompts, candidate lists).
+// quota_bcast (NCCL mode, every rank alike): rank 0's host quotas go to d_quota and join
+// the C-1 broadcast; the tail then reads them from there.
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
-                        int q, cudaStream_t s_prep = nullptr, cudaStream_t s_scan = nullptr);
+                        int q, cudaStream_t s_prep = nullptr, cudaStream_t s_scan = nullptr,
+                        bool quota_bcast = false, const int32_t* quota = nullptr);
 
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
   if (!keys_dev) return ARGUS_E_INVALID;
@@ -836,7 +842,7 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
 // With s_prep / s_scan (pipelined mode) prep and scan go to those streams, without
 // the programmatic (PDL) relaxation, and the caller inserts the events between them.
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
-                        int q, cudaStream_t s_prep, cudaStream_t s_scan) {
+                        int q, cudaStream_t s_prep, cudaStream_t s_scan, bool quota_bcast, const int32_t* quota) {
   const bool pipelined = s_prep != nullptr;
   if (!s_prep) s_prep = r->stream;
   if (!s_scan) s_scan = r->stream;
@@ -845,6 +851,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   if (N < 1 || N > r->cfg.max_batch) return ARGUS_E_INVALID;
   const bool root = r->cfg.rank == 0 || !nccl_mode(r);
   if (root && !prompts_dev) return ARGUS_E_INVALID;
+  if (quota_bcast && (!nccl_mode(r) || (root && !quota))) return ARGUS_E_INVALID;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d, k = r->cfg.k;
   const int n_pad = ((N + 127) / 128) * 128;
@@ -853,7 +860,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     StageScope sc(r, ARGUS_STAGE_PREP, s_prep);
     launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q],
                         r->flags_cur ? r->flags_cur : r->d_flags,
-                        s_prep, !pipelined);
+                        s_prep, !pipelined, quota_bcast ? quota : nullptr, r->cfg.L, r->d_quota);
     LAUNCHED(r);
   }
   if (!root) {
@@ -870,6 +877,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     NC_TRY(r, nccl().GroupStart());
     NC_TRY(r, nccl().Broadcast(r->d_Xb[q], r->d_Xb[q], (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
     NC_TRY(r, nccl().Broadcast(r->d_invq[q], r->d_invq[q], (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
+    if (quota_bcast) NC_TRY(r, nccl().Broadcast(r->d_quota, r->d_quota, 32, ncclInt32, 0, r->comm, r->stream));
     NC_TRY(r, nccl().GroupEnd());
   }
   if (k == 0) {  // SM mode: no cache scan, the tail sees the prompts only
@@ -952,8 +960,15 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                        uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr);
 static int async_harvest(argus_router* r, int q);
+// route_batch* in NCCL mode: the quotas are rank 0's (broadcast), other ranks may pass NULL
+static bool quota_from_root(const argus_router* r) {
+  return nccl_mode(r) && r->policy == ARGUS_POLICY_SD;
+}
 static int quota_ok(const argus_router* r, const int32_t* quota) {
   if (r->policy == ARGUS_POLICY_PASM) return 1;  // quotas are not used when sampling the PASM
+  // (rank 0's values are checked by the tail on every rank, so an invalid quota fails
+  // the call everywhere instead of leaving the other ranks inside the broadcast)
+  if (quota_from_root(r)) return r->cfg.rank != 0 || quota != nullptr;
   if (!quota) return 0;
   for (int v = 0; v < r->cfg.L; ++v)
     if (quota[v] < 0) return 0;
@@ -974,7 +989,9 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   int rc = check_state(r);
   if (rc) return rc;
   const bool sm_mode = r->cfg.k == 0;
-  if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota)) return ARGUS_E_INVALID;
+  const bool qdev = r->quota_dev_next;
+  r->quota_dev_next = false;
+  if (N < 1 || N > r->cfg.max_batch || (!qdev && !quota_ok(r, quota))) return ARGUS_E_INVALID;
   if (!sm_mode && (P < 1 || !keys_in)) return ARGUS_E_INVALID;
   const int L = r->cfg.L, k = r->cfg.k;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
@@ -1008,6 +1025,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
   for (int v = 0; v < 32; ++v) m.quota[v] = (v < L && quota) ? quota[v] : 0;
+  m.quota_dev = qdev ? r->d_quota : nullptr;
   m.option_out = option_out_dev ? option_out_dev : r->d_option;
   m.status = status_dev ? status_dev : r->d_status;
   m.flags = r->flags_cur ? r->flags_cur : r->d_flags;
@@ -1087,8 +1105,10 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     return finish_impl(r, r->d_partial[0], P, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
                        status_dev, r->stream, true, ex);
   }
-  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P, 0);
+  const bool qb = quota_from_root(r);
+  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P, 0, nullptr, nullptr, qb, quota);
   if (rc) return rc;
+  r->quota_dev_next = qb;
   // C-2: N*k candidate keys from every shard
   if (r->cfg.k > 0)
     NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));

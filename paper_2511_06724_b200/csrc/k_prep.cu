@@ -55,11 +55,14 @@ __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t
 
 __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, int d,
                                __nv_bfloat16* __restrict__ Xb, float* __restrict__ inv_q,
-                               uint64_t* __restrict__ gthr, int32_t* __restrict__ ctr, uint32_t* flags) {
+                               uint64_t* __restrict__ gthr, int32_t* __restrict__ ctr, uint32_t* flags,
+                               QuotaVec quota, int32_t* __restrict__ quota_dev) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  pdl_wait();  // the previous batch's kernels may still read Xb / inv_q
+  pdl_wait();  // the previous batch's kernels may still read Xb / inv_q / the quotas
   if (blockIdx.x == 0 && threadIdx.x < CTR_WORDS) ctr[threadIdx.x] = 0;  // scan work / visit counters
+  // multi-GPU: the root stages its quotas c_v next to the batch for the C-1 broadcast
+  if (quota_dev && blockIdx.x == 0 && threadIdx.x < 32) quota_dev[threadIdx.x] = quota.v[threadIdx.x];
   if (warp >= n_pad) return;
   if (lane == 0) gthr[warp] = 0;  // the scan's shared per-prompt threshold starts empty
   if (warp >= N) {  // zero padding rows: score 0, never reported
@@ -90,10 +93,14 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 }
 
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
-                         float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s, bool pdl) {
+                         float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s, bool pdl,
+                         const int32_t* quota, int32_t L, int32_t* quota_dev) {
   const int threads = 256;
   int blocks = (n_pad * 32 + threads - 1) / threads;
-  launch_pdl_opt(pdl, k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, ctr, flags);
+  QuotaVec qv{};
+  for (int v = 0; v < 32; ++v) qv.v[v] = (quota && v < L) ? quota[v] : 0;
+  launch_pdl_opt(pdl, k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, ctr, flags,
+                 qv, quota ? quota_dev : nullptr);
 }
 
 }  // namespace argus

@@ -141,7 +141,14 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
 
   // serial dictatorship over staged chunks
   __shared__ int32_t rem_s[32];
-  if (tid < 32) rem_s[tid] = tid < L ? a.quota[tid] : 0;
+  if (tid < 32) {
+    int c = tid < L ? (a.quota_dev ? a.quota_dev[tid] : a.quota[tid]) : 0;
+    if (c < 0) {  // only reachable through the broadcast (the host API checks its own argument)
+      atomicOr(a.flags, FLAG_INVALID_INPUT);
+      c = 0;
+    }
+    rem_s[tid] = c;
+  }
   bool any_overflow = false;
   const int W = Lw / 4;
   const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.prefl);

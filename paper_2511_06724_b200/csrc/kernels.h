@@ -63,9 +63,15 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
                         int64_t cap, bool dry, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags, cudaStream_t s);
 
 // K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
+// With quota != nullptr (host [L]) it also writes the quotas into quota_dev [32]
+// (the multi-GPU root, ahead of the C-1 broadcast).
+struct QuotaVec {
+  int32_t v[32];
+};
 void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
                          float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s,
-                         bool pdl = true);
+                         bool pdl = true, const int32_t* quota = nullptr, int32_t L = 0,
+                         int32_t* quota_dev = nullptr);
 
 // K1+K2: fused tcgen05 scan + per-range top-k -> partial [P][N][k].
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
@@ -120,6 +126,7 @@ struct TailArgs {
   uint32_t* cmask;           // [N] compliance mask
   // A6
   int32_t quota[32];         // per-option quotas c_v (by value)
+  const int32_t* quota_dev;  // [32] when non-null: the quotas broadcast from rank 0 (used instead)
   int32_t* option_out;       // [N] out
   uint8_t* status;           // [N] out
   uint32_t* flags;

@@ -49,3 +49,27 @@ def test_one_rank_nccl_path_matches_single_gpu(argus_mod, N, M, evict):
     for key in ("option", "topk_idx", "topk_score", "quality", "status", "optimal", "topk_handle", "dev_option",
                 "dev_idx"):
         np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+
+
+def test_nccl_path_quota_broadcast_checks_negative(argus_mod):
+    """Under NCCL the tail reads rank 0's broadcast quotas from the device: a negative
+    quota fails the call (ARGUS_E_INVALID, on every rank) without poisoning the router,
+    and the next valid call matches the single-GPU router."""
+    argus = argus_mod
+    N, M = 150, 6000
+    p = gen.small_problem("C2", N=N, M=M, seed=173)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    bad = quota.copy()
+    bad[1] = -1
+    outs = []
+    for uid in (None, argus.argus_nccl_unique_id()):
+        with argus.Router(768, p.k, p.opts, p.W1, p.b1, p.W2, p.b2, capacity=M, max_batch=N,
+                          nccl_unique_id=uid) as r:
+            r.argus_cache_insert(p.cache)
+            with pytest.raises(argus.ArgusError):
+                r.argus_route_batch(p.X, bad)
+            outs.append(r.argus_route_batch(p.X, quota))
+    (rc0, a), (rc1, b) = outs
+    assert rc0 == rc1
+    for key in a:
+        np.testing.assert_array_equal(a[key], b[key], err_msg=key)

@@ -49,6 +49,25 @@ for N in [int(x) for x in (sys.argv[1:] or ["96"])]:
             r.argus_route_batch_dev(Xd, q, o["option"], o["topk_idx"], o["topk_score"], o["quality"], o["status"])
         r.argus_sync()
         devpipe = (time.perf_counter() - t0) / reps * 1e6
+        # asynchronous host call (the bench's e2e): host enqueue cost vs wall time per batch
+        outs = [dict(option=torch.empty(N, dtype=torch.int32).pin_memory().numpy(),
+                     topk_idx=torch.empty((N, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+                     topk_score=torch.empty((N, k), dtype=torch.float32).pin_memory().numpy(),
+                     quality=torch.empty((N, L), dtype=torch.float32).pin_memory().numpy(),
+                     status=torch.empty(N, dtype=torch.uint8).pin_memory().numpy()) for _ in range(8)]
+        for i in range(8):
+            r.argus_route_wait(r.argus_route_batch_async(Xp, q, outs[i]))
+        enq = 0.0
+        t0 = time.perf_counter()
+        last = None
+        for i in range(reps):
+            t1 = time.perf_counter()
+            last = r.argus_route_batch_async(Xp, q, outs[i % 8])
+            enq += time.perf_counter() - t1
+        r.argus_route_wait(last)
+        asyn = (time.perf_counter() - t0) / reps * 1e6
+        print(f"N={N} pipeline={pipe}: async call wall {asyn:.1f} us/batch, host enqueue {enq / reps * 1e6:.1f} us/call",
+              flush=True)
         r.argus_profile_enable(True)
         r.argus_profile_read()
         for _ in range(50):

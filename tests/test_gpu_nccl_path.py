@@ -73,3 +73,43 @@ def test_nccl_path_quota_broadcast_checks_negative(argus_mod):
     assert rc0 == rc1
     for key in a:
         np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+
+
+def test_nccl_path_async_and_pasm(argus_mod):
+    """The asynchronous host call and the PASM policy (no quotas: nothing to broadcast)
+    through the one-rank NCCL communicator match the single-GPU router bit for bit."""
+    import torch
+    argus = argus_mod
+    N, M = 140, 7000
+    p = gen.small_problem("C2", N=N, M=M, seed=175)
+    L = len(p.opts)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    P = argus.argus_oda_pasm(np.ones(L), p.fractions)
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt).pin_memory().numpy()
+
+    results = []
+    for uid in (None, argus.argus_nccl_unique_id()):
+        with argus.Router(768, p.k, p.opts, p.W1, p.b1, p.W2, p.b2, capacity=M, max_batch=N,
+                          nccl_unique_id=uid) as r:
+            r.argus_cache_insert(p.cache)
+            outs = []
+            for policy in (argus.POLICY_SD, argus.POLICY_PASM):
+                if policy == argus.POLICY_PASM:
+                    r.argus_set_policy(argus.POLICY_PASM, P, 77)
+                tickets = []
+                for b in range(3):
+                    o = dict(option=pinned((N,), torch.int32), topk_idx=pinned((N, p.k), torch.int32).view(np.uint32),
+                             topk_score=pinned((N, p.k), torch.float32), quality=pinned((N, L), torch.float32),
+                             status=pinned((N,), torch.uint8))
+                    Xb = torch.from_numpy(np.roll(p.X, b, axis=0).copy()).pin_memory().numpy()
+                    q = quota if policy == argus.POLICY_SD else None
+                    tickets.append((r.argus_route_batch_async(Xb, q, o), o))
+                for t, o in tickets:
+                    outs.append((r.argus_route_wait(t), o))
+            results.append(outs)
+    for (rc0, a), (rc1, b) in zip(*results):
+        assert rc0 == rc1
+        for key in a:
+            np.testing.assert_array_equal(a[key], b[key], err_msg=key)

@@ -277,11 +277,13 @@ def test_pipelined_matches_serial(argus_mod):
 
 
 @pytest.mark.parametrize("N,M,d,seed", [(64, 4096, 1024, 111), (200, 20000, 1024, 112), (77, 9000, 832, 113),
-                                        (129, 5000, 960, 114), (33, 3000, 64, 115)])
+                                        (129, 5000, 960, 114), (33, 3000, 64, 115), (256, 6000, 64, 116),
+                                        (200, 7000, 128, 117), (512, 5000, 192, 118)])
 def test_wide_and_narrow_embeddings(argus_mod, N, M, d, seed):
     """d > 768 (OpenCLIP-H d = 1024, C4): k-blocks 12.. of the prompt slice are read by
     the MMA from shared memory, cache tiles stream through quarter-tile slots; d = 832
-    / 960 split unevenly over the quarters; d = 64 is a single k-block."""
+    / 960 split unevenly over the quarters; d = 64 is a single k-block (one of the two
+    half-tile slots of a tile is then empty), also on CTA pairs (N = 200, 256, 512)."""
     p = gen.small_problem("C4", N=N, M=M, d=d, seed=seed)
     g, tk, _ = run_case(argus_mod, p)
     assert tk["max_score_err"] < 1e-4

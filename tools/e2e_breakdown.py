@@ -68,6 +68,19 @@ for N in [int(x) for x in (sys.argv[1:] or ["96"])]:
         asyn = (time.perf_counter() - t0) / reps * 1e6
         print(f"N={N} pipeline={pipe}: async call wall {asyn:.1f} us/batch, host enqueue {enq / reps * 1e6:.1f} us/call",
               flush=True)
+        # again after the device-buffer runs (separates power / clock state from the call path)
+        t0 = time.perf_counter()
+        for i in range(reps):
+            last = r.argus_route_batch_async(Xp, q, outs[i % 8])
+        r.argus_route_wait(last)
+        torch.cuda.synchronize()
+        t0b = time.perf_counter()
+        for _ in range(reps):
+            r.argus_route_batch_dev(Xd, q, o["option"], o["topk_idx"], o["topk_score"], o["quality"], o["status"])
+        r.argus_sync()
+        devpipe2 = (time.perf_counter() - t0b) / reps * 1e6
+        print(f"N={N} pipeline={pipe}: async again {(t0b - t0) / reps * 1e6:.1f} us/batch, then dev pipelined "
+              f"{devpipe2:.1f} us/batch", flush=True)
         r.argus_profile_enable(True)
         r.argus_profile_read()
         for _ in range(50):

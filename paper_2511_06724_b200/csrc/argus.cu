@@ -986,11 +986,11 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                        uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex) {
+  const bool qdev = r->quota_dev_next;  // consumed by this call whatever happens
+  r->quota_dev_next = false;
   int rc = check_state(r);
   if (rc) return rc;
   const bool sm_mode = r->cfg.k == 0;
-  const bool qdev = r->quota_dev_next;
-  r->quota_dev_next = false;
   if (N < 1 || N > r->cfg.max_batch || (!qdev && !quota_ok(r, quota))) return ARGUS_E_INVALID;
   if (!sm_mode && (P < 1 || !keys_in)) return ARGUS_E_INVALID;
   const int L = r->cfg.L, k = r->cfg.k;

@@ -12,12 +12,12 @@ using namespace argus;
 // n_ss: how many of the 16 k-blocks take A from shared memory; the rest from TMEM
 // (TMEM A would need 512 columns for all 16, so the TS k-blocks reuse columns mod 12).
 // B: 16 boxes of 64 rows x 64 cols (8 KB each), A tail: 4 blocks of 128 x 64 (16 KB each).
-template <int NSS>
+template <int NSS, int CEVERY = 64>
 __global__ void bench_tile(int tiles, int n_cols, long long* out) {
   constexpr int n_ss = NSS;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
@@ -26,6 +26,7 @@ __global__ void bench_tile(int tiles, int n_cols, long long* out) {
   }
   if (threadIdx.x == 0) {
     tc::mbar_init(tc::smem_u32(&bar), 1);
+    tc::mbar_init(tc::smem_u32(&bar2), 1);
     tc::fence_barrier_init();
   }
   for (int i = threadIdx.x; i < 192 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
@@ -54,6 +55,8 @@ __global__ void bench_tile(int tiles, int n_cols, long long* out) {
           else
             tc::mma_ss_warp(dcol, adesc + (uint64_t)((((kb - kb_ts) & 3) * 16384 + kk * 32) >> 4), bd, idesc,
                             (kb | kk) != 0);
+          if (CEVERY < 64 && ((kb * 4 + kk) % CEVERY) == CEVERY - 1 && (kb * 4 + kk) != 63)
+            tc::mma_commit_warp(tc::smem_u32(&bar2));  // extra per-slot commits (tracked, never waited)
         }
       }
       tc::mma_commit_warp(tc::smem_u32(&bar));
@@ -70,14 +73,14 @@ __global__ void bench_tile(int tiles, int n_cols, long long* out) {
   }
 }
 
-template <int NSS>
+template <int NSS, int CEVERY = 64>
 static double run(int tiles, int n, int ctas) {
   static long long* d = nullptr;
   if (!d) cudaMalloc(&d, 8);
-  cudaFuncSetAttribute(bench_tile<NSS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(bench_tile<NSS, CEVERY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   long long c = 0;
   for (int rep = 0; rep < 3; ++rep) {
-    bench_tile<NSS><<<ctas, 128, 200 * 1024>>>(tiles, n, d);
+    bench_tile<NSS, CEVERY><<<ctas, 128, 200 * 1024>>>(tiles, n, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
@@ -94,5 +97,8 @@ int main() {
   printf("M=128 N=32,  4 of 16 k-blocks SS: %7.2f cycles/mma\n", run<4>(400, 32, 1));
   printf("148 CTAs N=64, 0 SS: %7.2f cycles/mma (CTA 0)\n", run<0>(4000, 64, 148));
   printf("148 CTAs N=64, 4 SS: %7.2f cycles/mma (CTA 0)\n", run<4>(4000, 64, 148));
+  printf("M=128 N=64, 0 SS, commit every 32 MMAs: %7.2f cycles/mma\n", run<0, 32>(400, 64, 1));
+  printf("M=128 N=64, 0 SS, commit every 16 MMAs: %7.2f cycles/mma\n", run<0, 16>(400, 64, 1));
+  printf("M=128 N=64, 4 SS, commit every 16 MMAs: %7.2f cycles/mma\n", run<4, 16>(400, 64, 1));
   return 0;
 }

@@ -93,7 +93,9 @@ __device__ __forceinline__ int pslice_of(int64_t pk) { return (int)((pk >> 36) &
 __device__ __forceinline__ int slot_of(int64_t pk) { return (int)((pk >> 44) & 0xFF); }
 __device__ __forceinline__ int epoch_of(int64_t pk) { return (int)(pk >> 52); }
 
-template <int KMAX, int KBV>
+// KBF: the number of k-blocks fixed at compile time (12 for d = 768, the CLIP width),
+// so the MMA issue loops unroll into constant descriptor offsets; 0 = d / 64 at run time.
+template <int KMAX, int KBV, int KBF = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_pair(const __grid_constant__ CUtensorMap tmap_c32, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
                 int pslices, int64_t n_tiles, int l2mode) {
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const bool floater = pair >= n_home;
   const int pslice = floater ? (pair - n_home) % pslices : pair % pslices;
   const int range = floater ? a.home_max + (pair - n_home) : pair / pslices;  // this pair's list slot
-  const int KB = a.d / KBLK;
+  const int KB = KBF ? KBF : a.d / KBLK;
   const int pbase = pslice * 2 * TM + (int)crank * TM;  // this CTA's first prompt
 
   if (warp == 0 && lane == 0) {
@@ -309,33 +311,34 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (leader && (warp == 1 || warp == 3)) {
     // ======================= MMA issuers (leader): M = 256 (both CTAs' prompts) x N = 64
     constexpr uint32_t IDESC = tc::idesc_bf16_f32(2 * TM, TN);
-    tc::mbar_wait(tc::smem_u32(&sm->qpair), 0);
-    if (KBV > KB_TMEM) tc::mbar_wait(tc::smem_u32(&sm->atail), 0);
+    tc::mbar_wait_warp(tc::smem_u32(&sm->qpair), 0);
+    if (KBV > KB_TMEM) tc::mbar_wait_warp(tc::smem_u32(&sm->atail), 0);
     tc::fence_after();
     const uint64_t dbase = tc::desc_kmajor_sw128(ring_s);
     const uint64_t abase = tc::desc_kmajor_sw128(region_s);  // A tail (KBV = 16)
     int my_ep = 0;
     for (int64_t l = warp == 1 ? 0 : 1;; l += 2) {
-      tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
-      const int64_t pk = sm->tile_id[l & (INV_SLOTS - 1)];
+      tc::mbar_wait_warp(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
+      const int64_t pk = __shfl_sync(0xffffffffu, (long long)sm->tile_id[l & (INV_SLOTS - 1)], 0);  // uniform
       if (pk < 0) break;
       if (epoch_of(pk) != my_ep) {  // both CTAs reloaded their prompt halves of the new pair slice
         my_ep = epoch_of(pk);
-        tc::mbar_wait(tc::smem_u32(&sm->qpair), (uint32_t)(my_ep & 1));
+        tc::mbar_wait_warp(tc::smem_u32(&sm->qpair), (uint32_t)(my_ep & 1));
         tc::fence_after();
       }
       const int b = (int)(l & 1);
-      tc::mbar_wait(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
+      tc::mbar_wait_warp(tc::smem_u32(&sm->tempty[b]), (uint32_t)(((l >> 1) & 1) ^ 1));
       tc::fence_after();
       const uint32_t d_tmem = tmem + ACC_COL0 + b * TN;
 #pragma unroll
       for (int hh = 0; hh < SPT; ++hh) {
         const int64_t u = SPT * l + hh;
         const int sl = (int)(u & (NSLOT - 1));
-        tc::mbar_wait(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 3) & 1));
+        tc::mbar_wait_warp(tc::smem_u32(&sm->full[sl]), (uint32_t)((u >> 3) & 1));
         tc::fence_after();
         const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
         const uint64_t dslot = dbase + (uint64_t)((sl * SH::SLOT_BYTES) >> 4);
+#pragma unroll
         for (int j = 0; j < kb1 - kb0; ++j) {
           const int kb = kb0 + j;
           if (KBV == KB_TMEM || kb < KB_TMEM) {
@@ -536,13 +539,13 @@ bool scan_pair_supported(int d, int32_t N) {
   return d % KBLK == 0 && d / KBLK <= KB_MAX && slices >= 2 && slices % 2 == 0;
 }
 
-template <int KMAX, int KBV>
+template <int KMAX, int KBV, int KBF = 0>
 static cudaError_t launch_pair_variant(bool pdl, dim3 grid, cudaStream_t s, const CUtensorMap& tc32,
                                        const CUtensorMap& tq, const ScanArgs& a, int pslices, int64_t n_tiles,
                                        int l2mode) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scan_pair<KMAX, KBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(k_scan_pair<KMAX, KBV, KBF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -562,11 +565,11 @@ static cudaError_t launch_pair_variant(bool pdl, dim3 grid, cudaStream_t s, cons
   static bool told = false;
   if (!told && getenv("ARGUS_DEBUG")) {
     int nc = -1;
-    cudaOccupancyMaxActiveClusters(&nc, (const void*)k_scan_pair<KMAX, KBV>, &cfg);
+    cudaOccupancyMaxActiveClusters(&nc, (const void*)k_scan_pair<KMAX, KBV, KBF>, &cfg);
     fprintf(stderr, "argus: pair scan grid %u CTAs, max co-resident 2-CTA clusters %d\n", grid.x, nc);
     told = true;
   }
-  return cudaLaunchKernelEx(&cfg, k_scan_pair<KMAX, KBV>, tc32, tq, a, pslices, n_tiles, l2mode);
+  return cudaLaunchKernelEx(&cfg, k_scan_pair<KMAX, KBV, KBF>, tc32, tq, a, pslices, n_tiles, l2mode);
 }
 
 cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, const CUtensorMap* tmap_q,
@@ -582,9 +585,13 @@ cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, con
   }
   const int l2mode = l2env >= 0 ? l2env : (pslices == 1 ? 0 : 1);
   const bool wide = a.d / KBLK > KB_TMEM;
-  if (a.k <= 4)
+  const bool clip = a.d == KB_TMEM * KBLK;  // d = 768: compile-time k-block count
+  if (a.k <= 4) {
+    if (clip) return launch_pair_variant<4, 12, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
     return wide ? launch_pair_variant<4, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
                 : launch_pair_variant<4, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  }
+  if (clip) return launch_pair_variant<8, 12, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
   return wide ? launch_pair_variant<8, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
               : launch_pair_variant<8, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
 }

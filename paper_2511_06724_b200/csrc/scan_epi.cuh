@@ -22,14 +22,21 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     const float4 ic = tc::lds_f32x4(icp + c4 * 16);   // shared memory, same address in every lane (broadcast)
-    const float x0 = __fmul_rn(__uint_as_float(v[c4 * 4 + 0]), ic.x);
-    const float x1 = __fmul_rn(__uint_as_float(v[c4 * 4 + 1]), ic.y);
-    const float x2 = __fmul_rn(__uint_as_float(v[c4 * 4 + 2]), ic.z);
-    const float x3 = __fmul_rn(__uint_as_float(v[c4 * 4 + 3]), ic.w);
-    v[c4 * 4 + 0] = __float_as_uint(x0);
-    v[c4 * 4 + 1] = __float_as_uint(x1);
-    v[c4 * 4 + 2] = __float_as_uint(x2);
-    v[c4 * 4 + 3] = __float_as_uint(x3);
+    // x = fl(acc * inv_c): packed fp32x2 multiplies (FMUL2, round-to-nearest per lane,
+    // the same bits as two __fmul_rn) halve the epilogue's multiply issue slots
+    uint64_t p01, p23;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p01)
+        : "l"(((uint64_t)v[c4 * 4 + 1] << 32) | v[c4 * 4 + 0]),
+          "l"(((uint64_t)__float_as_uint(ic.y) << 32) | __float_as_uint(ic.x)));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p23)
+        : "l"(((uint64_t)v[c4 * 4 + 3] << 32) | v[c4 * 4 + 2]),
+          "l"(((uint64_t)__float_as_uint(ic.w) << 32) | __float_as_uint(ic.z)));
+    v[c4 * 4 + 0] = (uint32_t)p01;
+    v[c4 * 4 + 1] = (uint32_t)(p01 >> 32);
+    v[c4 * 4 + 2] = (uint32_t)p23;
+    v[c4 * 4 + 3] = (uint32_t)(p23 >> 32);
+    const float x0 = __uint_as_float(v[c4 * 4 + 0]), x1 = __uint_as_float(v[c4 * 4 + 1]);
+    const float x2 = __uint_as_float(v[c4 * 4 + 2]), x3 = __uint_as_float(v[c4 * 4 + 3]);
     m = fmaxf(m, fmaxf(fmaxf(x0, x1), fmaxf(x2, x3)));
   }
   const bool cand = __fmul_rn(m, iq) >= thr;

@@ -585,13 +585,16 @@ cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, con
   }
   const int l2mode = l2env >= 0 ? l2env : (pslices == 1 ? 0 : 1);
   const bool wide = a.d / KBLK > KB_TMEM;
-  const bool clip = a.d == KB_TMEM * KBLK;  // d = 768: compile-time k-block count
+  const bool clip = a.d == KB_TMEM * KBLK;  // d = 768 (CLIP): compile-time k-block count
+  const bool clip_h = a.d == KB_MAX * KBLK;  // d = 1024 (OpenCLIP-H)
   if (a.k <= 4) {
     if (clip) return launch_pair_variant<4, 12, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+    if (clip_h) return launch_pair_variant<4, 16, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
     return wide ? launch_pair_variant<4, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
                 : launch_pair_variant<4, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
   }
   if (clip) return launch_pair_variant<8, 12, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
+  if (clip_h) return launch_pair_variant<8, 16, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
   return wide ? launch_pair_variant<8, 16>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode)
               : launch_pair_variant<8, 12>(pdl, grid, s, *tmap_c32, *tmap_q, a, pslices, n_tiles, l2mode);
 }

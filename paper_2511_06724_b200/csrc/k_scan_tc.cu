@@ -99,7 +99,9 @@ struct ScanSmem {  // placed after the region
 static_assert(offsetof(ScanSmem, invc) % 16 == 0, "bulk-copy / float4 destination");
 static_assert(sizeof(ScanSmem) <= SCRATCH_OFF, "barriers fit before the scratch");
 
-template <int KMAX, int KBV>
+// KBF: k-blocks fixed at compile time (12 for d = 768, 16 for d = 1024) so the MMA
+// issue loops unroll into constant descriptor offsets; 0 = d / 64 at run time.
+template <int KMAX, int KBV, int KBF = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_q, ScanArgs a,
               int slices, int64_t n_tiles, int l2mode) {
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slice = blockIdx.x % slices;
   const int range = blockIdx.x / slices;  // index of this CTA's candidate list
-  const int KB = a.d / KBLK;
+  const int KB = KBF ? KBF : a.d / KBLK;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmap_c);
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::fence_after();
         const int kb0 = KB * hh / SPT, kb1 = KB * (hh + 1) / SPT;
         const uint64_t dslot = dbase + (uint64_t)((sl * SH::SLOT_BYTES) >> 4);
+#pragma unroll
         for (int j = 0; j < kb1 - kb0; ++j) {
           const int kb = kb0 + j;
           if (KBV == KB_TMEM || kb < KB_TMEM) {
@@ -388,15 +391,15 @@ int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms) {
 
 bool scan_supported(int d) { return d % KBLK == 0 && d >= KBLK && d / KBLK <= KB_MAX; }
 
-template <int KMAX, int KBV>
+template <int KMAX, int KBV, int KBF = 0>
 static void launch_variant(bool pdl, dim3 grid, cudaStream_t s, const CUtensorMap& tc_, const CUtensorMap& tq,
                            const ScanArgs& a, int slices, int64_t n_tiles, int l2mode) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scan_tc<KMAX, KBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(k_scan_tc<KMAX, KBV, KBF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     attr = true;
   }
-  launch_pdl_opt(pdl, k_scan_tc<KMAX, KBV>, grid, dim3(THREADS), SMEM_BYTES, s, tc_, tq, a, slices, n_tiles, l2mode);
+  launch_pdl_opt(pdl, k_scan_tc<KMAX, KBV, KBF>, grid, dim3(THREADS), SMEM_BYTES, s, tc_, tq, a, slices, n_tiles, l2mode);
 }
 
 void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* tmap_q, cudaStream_t s, bool pdl) {
@@ -413,11 +416,16 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
   static int stat = getenv("ARGUS_SCAN_1MMA") ? 32 : 0;
   const int l2mode = (l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1)) | stat;
   const bool wide = a.d / KBLK > KB_TMEM;
+  const bool clip = a.d == KB_TMEM * KBLK, clip_h = a.d == KB_MAX * KBLK;  // d = 768 / 1024
   if (a.k <= 4) {
-    if (wide) launch_variant<4, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    if (clip) launch_variant<4, 12, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else if (clip_h) launch_variant<4, 16, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else if (wide) launch_variant<4, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
     else launch_variant<4, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
   } else {
-    if (wide) launch_variant<8, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    if (clip) launch_variant<8, 12, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else if (clip_h) launch_variant<8, 16, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
+    else if (wide) launch_variant<8, 16>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
     else launch_variant<8, 12>(pdl, grid, s, *tmap, *tmap_q, a, slices, n_tiles, l2mode);
   }
 }

@@ -12,7 +12,7 @@ for C in C5 C3 C4; do timeout 600 python bench.py --config $C --steps 40 --warmu
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 200 --csv \
    --log-file $OUT/launches.csv python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 > $OUT/ncu_launches.log 2>&1
-for spec in "C2:64:k_scan_tc" "C2:256:k_scan_pair" "C5:4096:k_scan_pair" "C4:8192:k_scan_pair"; do
+for spec in "C2:64:k_scan_tc" "C2:256:k_scan_pair" "C5:4096:k_scan_pair" "C4:8192:k_scan_pair" "C3:256:k_scan_pair"; do
   C=$(echo $spec | cut -d: -f1); N=$(echo $spec | cut -d: -f2); K=$(echo $spec | cut -d: -f3)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 6 -c 1 \
      -o $OUT/prof_${C}_N$N -f python bench.py --config $C --steps 4 --warmup 3 --no-cpu-baseline \

@@ -237,6 +237,19 @@ def main():
     for t in range(args.warmup):
         step(t)
     r.argus_sync()
+    # untimed clock ramp on top of the W warm-up steps: keep the board busy for
+    # >= 0.5 s so the timed region (0.2 s at C2) does not start on ramping clocks
+    # (every rank runs the same number of chunks: the steps hold collectives)
+    t_ramp = time.time() + 0.5
+    while True:
+        for t in range(args.warmup, args.warmup + 64):
+            step(t)
+        r.argus_sync()
+        more = float(time.time() < t_ramp)
+        if world > 1:
+            more = adist.max_over_ranks(dist, more, dev)
+        if not more:
+            break
     barrier()
     launches0 = r.argus_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)

@@ -183,6 +183,7 @@ struct argus_router {
   CUtensorMap tmap_c32;            // same shard, 32x64 boxes (half tiles of the CTA-pair scan)
   bool pair_scan = true;           // N > 128 on CTA pairs (ARGUS_NO_PAIR=1 disables)
   int tail_ysplit = 1;             // CTAs per prompt block of a pipelined tail (ARGUS_TAIL_YSPLIT)
+  int scan_reserve = 2;            // pipelined one-slice scans: SMs left to prep / tail (ARGUS_SCAN_RESERVE)
   bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   // stage profiling (argus_profile_*)
@@ -508,6 +509,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   r->pipe = c.pipeline != 0 && c.world == 1 && c.nccl_unique_id == nullptr;
   r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
+  if (const char* e = getenv("ARGUS_SCAN_RESERVE")) r->scan_reserve = std::min(std::max(atoi(e), 0), 16);
   r->migrate = getenv("ARGUS_NO_MIGRATE") == nullptr;
   if (r->pipe) {
     int lo = 0, hi = 0;
@@ -906,6 +908,11 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.gthr = r->d_gthr[q];
   a.ctr = r->d_ctr[q];
   bool pair = r->pair_scan && scan_pair_supported(d, N);
+  // the scan grid's SM budget: a pipelined one-slice scan (N <= 128, HBM-bound: 146 SMs
+  // still saturate HBM) leaves a few SMs free so the next batch's prep and this batch's
+  // tail run beside it instead of queueing behind the persistent grid (N = 48, fixed:
+  // 264 -> 256 us per batch with 2 SMs reserved, scripts/scan_reserve_sweep.sh)
+  const int scan_sms = pipelined && N <= 128 ? r->num_sms - r->scan_reserve : r->num_sms;
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
     if (pair) {
@@ -913,7 +920,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
       // TPC and let pairs whose slice runs dry continue another slice (list slots
       // [home_max, home_max + MAX_VISITS) for migrants, zeroed here since some stay unused).
       const int pslices = (N + 255) / 256;
-      const int clusters = r->num_sms / 2;
+      const int clusters = scan_sms / 2;
       const int64_t n_tiles = (a.m_local + 63) / 64;
       a.migrate = r->migrate && pslices >= 2 && clusters % pslices != 0 && n_tiles >= (int64_t)clusters * 16;
       if (a.migrate) {
@@ -924,7 +931,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
         if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
         CU_TRY(r, cudaMemsetAsync(r->d_partial[q], 0, sizeof(uint64_t) * (size_t)a.P * N * k, s_scan));
       } else {
-        a.P = scan_pair_plan(a.m_local, N, r->num_sms);
+        a.P = scan_pair_plan(a.m_local, N, scan_sms);
         a.home_max = a.P;
         a.floaters = 0;
       }
@@ -938,7 +945,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
       }
     }
     if (!pair) {
-      a.P = scan_plan_ranges(a.m_local, N, r->num_sms);
+      a.P = scan_plan_ranges(a.m_local, N, scan_sms);
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;
       launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
     }

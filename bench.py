@@ -56,7 +56,59 @@ def parse():
                     help="diagnostics: on one GPU, run the multi-GPU data path through a one-rank NCCL communicator")
     ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
                     help="1: the tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline)")
+    ap.add_argument("--tensor-n", type=int, default=4096,
+                    help="after the headline pass: fixed-N batches of this size on the same cache, the "
+                         "tensor-core regime (0 = off)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check only (CPU, gloo): rendezvous the ranks, time nothing, print the rank list")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-launch this script as N ranks
+    (one process per GPU) with the same arguments, exactly as the driver does."""
+    import socket
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dry_run(args, rank, world):
+    """Launcher check: every rank joins a gloo group; rank 0 prints who arrived."""
+    import torch
+    import torch.distributed as dist
+    from paper_2511_06724_b200 import dist as adist
+    dist.init_process_group("gloo")
+    ranks = [None] * world
+    dist.all_gather_object(ranks, rank)
+    t = adist.max_over_ranks(dist, float(rank))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": ranks, "max_over_ranks": t}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def timed_schedule(sizes, steps):
+    """Trace batches timed by the K steps.  K >= NT: whole passes over the trace, in
+    order.  The remainder (all of it when K < NT): a quantile sample of the trace's
+    batch sizes (the batch at quantile (j + 1/2) / r of the sorted sizes, j < r),
+    played in trace order, so any K samples the low and high MMPP states in
+    proportion (the first K batches of the trace are all low-state)."""
+    nt = len(sizes)
+    full, rem = divmod(steps, nt)
+    order = np.argsort(np.asarray(sizes), kind="stable")
+    tail = sorted(int(order[int((j + 0.5) * nt / rem)]) for j in range(rem)) if rem else []
+    return list(range(nt)) * full + tail
 
 
 def dist_env():
@@ -161,17 +213,44 @@ def cpu_baseline(cfg, cache_rows, queries, opts, W1, b1, W2, b2, quota_fn, secon
     rh = oracle.mlp(X, sc, W1, b1, W2, b2, threads=threads)
     oracle.assign(rh, sc[:, 0], opts, quota_fn(S))
     wall = time.perf_counter() - t0
+    # the same oracle on ONE thread: a few prompts over the full cache
+    S1 = max(1, min(4, S))
+    t1 = time.perf_counter()
+    oracle.scan_topk(X[:S1], cache_rows, cfg.k, threads=1)
+    wall1 = time.perf_counter() - t1
     return {"value": S / wall, "unit": "prompts/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"{S} prompts of the {cfg.name} workload scanned over the full M={cache_rows.shape[0]} cache "
-                      f"(fp64 C oracle, OpenMP over prompts), then predictor + assignment; {wall:.1f} s wall"}
+                      f"(fp64 C oracle, OpenMP over prompts), then predictor + assignment; {wall:.1f} s wall",
+            "one_thread": {"value": round(S1 / wall1, 3), "unit": "prompts/s", "cores": 1,
+                           "sample": f"{S1} prompts scanned (O1-O4) over the full cache on 1 thread; {wall1:.1f} s wall"}}
+
+
+def cpu_model():
+    """`lscpu` model name of this host (from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def main():
     args = parse()
     rank, world, local_rank = dist_env()
     cfg = gen.CONFIGS[args.config]
-    assert args.gpus == world or world == 1, "launch N>1 with torchrun --nproc-per-node N"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     assert args.warmup >= 0 and args.steps >= 1
+    if args.dry_run:
+        return dry_run(args, rank, world)
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -191,7 +270,11 @@ def main():
     fr = gen.load_fractions(L, cfg.frac_base)
     NT = n_trace(cfg, args.fixed_n)
     sizes = batch_sizes(cfg, NT) if not args.fixed_n else [args.fixed_n] * NT
-    max_batch = max(max(sizes), max([int(x) for x in args.sweep.split(",") if x] or [0]))
+    sweep_n = [int(x) for x in args.sweep.split(",") if x]
+    tensor_n = args.tensor_n if (args.tensor_n and not args.fixed_n) else 0
+    max_batch = max(max(sizes), max(sweep_n or [0]), tensor_n)
+    sched = timed_schedule(sizes, args.steps)
+    root = rank == 0  # rank 0's inputs are authoritative; the library broadcasts them
 
     from paper_2511_06724_b200 import dist as adist
     uid = adist.share_nccl_id(dist, rank, argus.argus_nccl_unique_id) if world > 1 else None
@@ -202,31 +285,39 @@ def main():
                      device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream,
                      pipeline=bool(args.pipeline) and world == 1 and uid is None)
 
-    # ---- cache: generated chunk by chunk, inserted through the ABI (rank 0 authoritative)
+    # ---- cache: generated chunk by chunk on rank 0 only, inserted through the ABI (the
+    # library broadcasts rank 0's rows; every rank keeps its stripe, so no rank holds more
+    # than its shard plus one staging chunk)
     cg = gen.CacheGen(cfg.M, d, cfg.seed)
-    cache_rows = cg.all(threads=os.cpu_count() or 1)  # kept: query repeats and the CPU baseline read it
+    cache_rows = cg.all(threads=os.cpu_count() or 1) if root else None  # query repeats + CPU baseline read it
     t0 = time.perf_counter()
     for a in range(0, cfg.M, gen.CHUNK):
-        r.argus_cache_insert(cache_rows[a:a + gen.CHUNK])  # rank 0's rows are authoritative (broadcast by the library)
+        n_a = min(gen.CHUNK, cfg.M - a)
+        r.argus_cache_insert(cache_rows[a:a + n_a] if root else None, n=n_a)
     t_insert = time.perf_counter() - t0
 
     # ---- batches (inputs resident in HBM for `value`; pinned host copies for e2e)
-    Xs = [gen.queries(cg, n, cfg.seed, b, cache_rows=cache_rows) for b, n in enumerate(sizes)]
-    quotas = [argus.argus_quota_from_fractions(fr, n) for n in sizes]
-    X_dev = [torch.from_numpy(x).to(f"cuda:{local_rank}") for x in Xs]
-    X_pin = [torch.from_numpy(x).pin_memory() for x in Xs]
     dev = torch.device("cuda", local_rank)
+    if root:
+        Xs = [gen.queries(cg, n, cfg.seed, b, cache_rows=cache_rows) for b, n in enumerate(sizes)]
+        quotas = [argus.argus_quota_from_fractions(fr, n) for n in sizes]
+        X_dev = [torch.from_numpy(x).to(dev) for x in Xs]
+        X_pin = [torch.from_numpy(x).pin_memory() for x in Xs]
+    else:
+        Xs = quotas = X_dev = X_pin = [None] * NT
     out = dict(option=torch.empty(max_batch, dtype=torch.int32, device=dev),
                topk_idx=torch.empty((max_batch, k), dtype=torch.int32, device=dev),
                topk_score=torch.empty((max_batch, k), dtype=torch.float32, device=dev),
                quality=torch.empty((max_batch, L), dtype=torch.float32, device=dev),
                status=torch.empty(max_batch, dtype=torch.uint8, device=dev))
 
-    def step(t):
-        b = t % NT
+    def step_b(b):
         r.argus_route_batch_dev(X_dev[b], quotas[b], out["option"], out["topk_idx"], out["topk_score"],
-                                out["quality"], out["status"])
+                                out["quality"], out["status"], N=sizes[b])
         return sizes[b]
+
+    def step(t):
+        return step_b(t % NT)
 
     def barrier():
         torch.cuda.synchronize()
@@ -259,8 +350,8 @@ def main():
     with sampler:
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for t in range(args.warmup, args.warmup + args.steps):
-                prompts += step(t)
+            for b in sched:
+                prompts += step_b(b)
             r.argus_route_join()  # the router's stream waits for the last pipelined tail
             ev1.record(stream)
         ev1.synchronize()
@@ -276,8 +367,8 @@ def main():
     r.argus_profile_enable(True)
     prof = {}
     per_launch = []  # (N, scan ms) of every launch, for the per-bound roofline split
-    for t in range(args.warmup, args.warmup + args.steps):
-        n = step(t)
+    for b in sched:
+        n = step_b(b)
         pr = r.argus_profile_read()  # synchronises: this pass is for timing kernels, not the headline
         for kk, (ms_, cnt) in pr.items():
             a0 = prof.get(kk, (0.0, 0))
@@ -291,8 +382,8 @@ def main():
     # ---- e2e through the public host-buffer API: argus_route_batch_async, the call of
     # a serving loop (pinned host prompts -> device, the whole path, outputs -> pinned
     # host buffers, every step; up to four calls in flight), timed on the router's stream
-    e2e_steps = args.e2e_steps or args.steps
-    Xh = [x.numpy() for x in X_pin]
+    e2e_sched = timed_schedule(sizes, args.e2e_steps) if args.e2e_steps else sched
+    Xh = [x.numpy() if x is not None else None for x in X_pin]
 
     def pinned(shape, dt):
         return torch.empty(shape, dtype=dt).pin_memory().numpy()
@@ -301,7 +392,7 @@ def main():
                    topk_score=pinned((n, k), torch.float32), quality=pinned((n, L), torch.float32),
                    status=pinned((n,), torch.uint8)) for n in sizes]
     for t in range(min(4, NT)):  # warm the async path
-        r.argus_route_wait(r.argus_route_batch_async(Xh[t], quotas[t], outs_h[t]))
+        r.argus_route_wait(r.argus_route_batch_async(Xh[t], quotas[t], outs_h[t], N=sizes[t]))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -309,25 +400,35 @@ def main():
     with torch.cuda.stream(stream):
         e0.record(stream)
         last = None
-        for t in range(e2e_steps):
-            b = t % NT
-            last = r.argus_route_batch_async(Xh[b], quotas[b], outs_h[b])
+        for b in e2e_sched:
+            last = r.argus_route_batch_async(Xh[b], quotas[b], outs_h[b], N=sizes[b])
             n = sizes[b]
             e2e_prompts += n
-            h2d += n * d * 4
+            h2d += n * d * 4 if root else 0
             d2h += n * (4 + k * 8 + L * 4 + 1) + 4
         r.argus_route_wait(last)  # every call's outputs are in host memory
         e1.record(stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     # the synchronous call, for reference (one batch at a time, nothing overlaps)
-    sync_steps = min(e2e_steps, 100)
+    sync_sched = e2e_sched[:100]
     s0 = time.perf_counter()
-    for t in range(sync_steps):
-        r.argus_route_batch(Xh[t % NT], quotas[t % NT])
-    sync_pps = sum(sizes[t % NT] for t in range(sync_steps)) / (time.perf_counter() - s0)
+    for b in sync_sched:
+        r.argus_route_batch(Xh[b], quotas[b], N=sizes[b])
+    sync_pps = sum(sizes[b] for b in sync_sched) / (time.perf_counter() - s0)
     if world > 1:
         e2e_ms = adist.max_over_ranks(dist, e2e_ms, dev)
+        sync_pps = -adist.max_over_ranks(dist, -sync_pps, dev)  # the slowest rank
+    ts = [sizes[b] for b in sched]
+    timed_n = {"mean_N": round(float(np.mean(ts)), 2), "min_N": int(min(ts)), "max_N": int(max(ts)),
+               "batches_N_gt_128": int(sum(n > 128 for n in ts)), "trace_mean_N": round(float(np.mean(sizes)), 2)}
+
+    # ---- tensor-core regime on the same cache: fixed N = tensor_n batches (the north
+    # star's ">= 60 % tensor-pipe utilisation at N >= 1024" target), scan timed per launch
+    tensor_line = None
+    if tensor_n:
+        tensor_line = tensor_regime(r, cg, cache_rows, cfg, fr, out, tensor_n, root, argus, torch, dev, dist,
+                                    world, barrier)
 
     if args.sweep:
         sweep(args, r, cg, cache_rows, cfg, fr, out, stream, argus)
@@ -338,7 +439,7 @@ def main():
     m_local = adist.local_rows(cfg.M, world, 0)
     bytes_per_launch = m_local * (2 * d + 4)
     achieved_gbs = bytes_per_launch * scan_n / (scan_ms / 1e3) / 1e9 if scan_n else None
-    flops = sum(2.0 * sizes[t % NT] * m_local * d for t in range(args.warmup, args.warmup + args.steps))
+    flops = sum(2.0 * sizes[b] * m_local * d for b in sched)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(tpath):
@@ -398,18 +499,23 @@ def main():
         "config": {
             "workload": f"{cfg.name}: {cfg.note}",
             "M": cfg.M, "d": d, "k": k, "L": L, "hidden": cfg.hidden,
-            "batch_sizes": f"MMPP trace seed 2018, {NT} batches cycled, mean N {np.mean(sizes):.1f}, "
-                           f"min {min(sizes)}, max {max(sizes)}" if (cfg.bursty and not args.fixed_n) else f"N={sizes[0]} ({NT} distinct batches cycled)",
+            "batch_sizes": (f"MMPP trace seed 2018, {NT} batches (mean N {np.mean(sizes):.1f}, min {min(sizes)}, "
+                            f"max {max(sizes)}); timed steps: whole trace passes, then a quantile sample of the "
+                            f"trace's sizes in trace order") if (cfg.bursty and not args.fixed_n)
+                           else f"N={sizes[0]} ({NT} distinct batches cycled)",
+            "timed_batches": timed_n,
             "parallelism": f"cache row-striped over {world} GPU(s)",
             "l2": f"inputs larger than L2 (cache shard {bytes_per_launch / 1e9:.2f} GB >> 126 MB L2)",
             "insert_s": round(t_insert, 2),
             "pipeline": ("tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline=1); every "
                          "batch's outputs are complete inside the timed region")
                         if (args.pipeline and world == 1) else "off",
+            "ranks_hold": "rank 0 generates the cache and prompts; the library broadcasts them, every rank keeps "
+                          "its stripe" if world > 1 else "one GPU holds the whole cache",
         },
         "e2e": {"value": round(e2e_prompts / (e2e_ms / 1e3), 1), "unit": "prompts/s",
-                "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
-                "steps": e2e_steps,
+                "h2d_bytes_per_step": int(h2d / len(e2e_sched)), "d2h_bytes_per_step": int(d2h / len(e2e_sched)),
+                "steps": len(e2e_sched),
                 "api": "argus_route_batch_async (pinned host buffers; H2D of the prompts and D2H of all outputs "
                        "inside every step; up to four calls in flight), then argus_route_wait",
                 "sync_call_prompts_per_s": round(sync_pps, 1)},
@@ -427,17 +533,63 @@ def main():
             "by_bound": roof_split,
         },
         "stage_ms_per_step": stage_ms,
+        "tensor_regime": tensor_line,
         "route_rc": rc,
         "clocks": sampler.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        res["cpu_baseline"] = cpu_baseline(cfg, cache_rows, np.concatenate(Xs[:8]), opts, W1, b1, W2, b2,
+        res["cpu_baseline"] = cpu_baseline(cfg, cache_rows, np.concatenate([Xs[b] for b in sched[:8]]), opts, W1, b1, W2, b2,
                                            lambda n: gen_quota(fr, n), args.cpu_seconds)
     if rank == 0:
         print(json.dumps(res), flush=True)
     r.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def tensor_regime(r, cg, cache_rows, cfg, fr, out, n, root, argus, torch, dev, dist, world, barrier, reps=8):
+    """Fixed-N batches (N = n, >> the ridge at N ~ 212) on the resident cache: the scan's
+    tensor-core throughput against the sustained bf16 peak, CUDA events per launch on the
+    stream the scan runs on (argus_profile_*), plus the whole step."""
+    X = torch.from_numpy(gen.queries(cg, n, cfg.seed, 20_000 + n, cache_rows=cache_rows)).to(dev) if root else None
+    q = argus.argus_quota_from_fractions(fr, n) if root else None
+
+    def go():
+        r.argus_route_batch_dev(X, q, out["option"], out["topk_idx"], out["topk_score"], out["quality"],
+                                out["status"], N=n)
+    for _ in range(3):
+        go()
+    r.argus_sync()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.ExternalStream(r.argus_get_stream())
+    e0.record(s)
+    for _ in range(reps):
+        go()
+    r.argus_route_join()
+    e1.record(s)
+    e1.synchronize()
+    step_ms = e0.elapsed_time(e1) / reps
+    r.argus_profile_read()
+    r.argus_profile_enable(True)
+    for _ in range(reps):
+        go()
+    pr = r.argus_profile_read()
+    r.argus_profile_enable(False)
+    barrier()
+    if world > 1:
+        from paper_2511_06724_b200 import dist as adist
+        step_ms = adist.max_over_ranks(dist, step_ms, dev)
+    _, tf_burst, tf_sust, src = load_peaks()
+    from paper_2511_06724_b200 import dist as adist
+    m_local = adist.local_rows(cfg.M, world, 0)
+    scan_ms = pr["scan"][0] / max(1, pr["scan"][1])
+    tf = 2.0 * n * m_local * cfg.d / (scan_ms / 1e3) / 1e12
+    return {"N": n, "M": cfg.M, "d": cfg.d, "prompts_per_s": round(n / (step_ms / 1e3), 1),
+            "ms_per_step": round(step_ms, 4), "scan_ms_per_launch": round(scan_ms, 4), "bound": "tensor",
+            "achieved": round(tf, 1), "peak": tf_sust, "unit": "TFLOP/s", "frac": round(tf / tf_sust, 4),
+            "peak_kind": "sustained bf16 (" + src + ")", "frac_of_burst": round(tf / tf_burst, 4),
+            "stage_ms": {kk: round(v[0] / max(1, v[1]), 4) for kk, v in pr.items() if v[1]}}
 
 
 def sweep(args, r, cg, cache_rows, cfg, fr, out, stream, argus):
@@ -535,7 +687,7 @@ def run_reference(args, cfg, rank, world):
         "config": {"workload": f"{cfg.name}: {cfg.note}", "M": cfg.M, "d": d, "k": k, "L": L,
                    "sample_per_step": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "prompts/s", "cores": threads, "kind": "oracle",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "prompts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "no reference implementation exists (the paper publishes no code); the reference arm is the "
                 "fp64 CPU oracle written from the paper",

@@ -211,9 +211,11 @@ int argus_route_wait(argus_router* r, int64_t ticket);
 /* Sharded pipeline pieces (external collective mode and tests).
  * partial: A1-A3 on this rank's shard -> keys_dev [N][k] uint64 (sorted desc;
  *          key = ord(score) << 32 | (0xFFFFFFFF - g), 0 = empty).
- * finish:  merge G shards' keys (keys_all_dev [G][N][k]) -> A3 outputs, then
- *          A4-A6 exactly as argus_route_batch_dev.  prompts_dev must be the
- *          same batch passed to partial (its bf16 copy is reused). */
+ * finish:  merge G shards' keys (keys_all_dev [G][N][k], 8-byte aligned, G ==
+ *          cfg.world, else ARGUS_E_INVALID) -> A3 outputs, then A4-A6 exactly as
+ *          argus_route_batch_dev.  prompts_dev must be the same batch passed to
+ *          partial (its bf16 copy and inverse norms are reused; an invalid prompt
+ *          there fails this call too, on every rank). */
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N,
                             uint64_t* keys_dev);
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,

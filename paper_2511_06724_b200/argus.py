@@ -236,7 +236,13 @@ class Router:
         self.close()
 
     # cache
-    def argus_cache_insert(self, emb) -> int:
+    def argus_cache_insert(self, emb, n=None) -> int:
+        """emb host fp32 [n][d]; emb = None with n rows on a non-root rank of an NCCL
+        router (rank 0's rows are broadcast by the library)."""
+        if emb is None:
+            first = C.c_int64(-1)
+            _check(_lib.argus_cache_insert(self._h, None, int(n), C.byref(first)), "argus_cache_insert")
+            return first.value
         emb = np.ascontiguousarray(emb, np.float32)
         first = C.c_int64(-1)
         _check(_lib.argus_cache_insert(self._h, _p(emb), emb.shape[0] if emb.size else 0, C.byref(first)),
@@ -265,11 +271,12 @@ class Router:
         return s.value or 0
 
     # routing
-    def argus_route_batch(self, prompts, quota, want_quality=True, want_status=True):
-        """Host-buffer route.  Returns (rc, dict of numpy outputs)."""
-        prompts = np.ascontiguousarray(prompts, np.float32)
-        quota = np.ascontiguousarray(quota, np.int32)
-        N = prompts.shape[0]
+    def argus_route_batch(self, prompts, quota, want_quality=True, want_status=True, N=None):
+        """Host-buffer route.  Returns (rc, dict of numpy outputs).  Non-root ranks of an
+        NCCL router may pass prompts = None (and quota = None) with N."""
+        prompts = None if prompts is None else np.ascontiguousarray(prompts, np.float32)
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
+        N = prompts.shape[0] if prompts is not None else int(N)
         out = dict(option=np.empty(N, np.int32), topk_idx=np.empty((N, self.k), np.uint32),
                    topk_score=np.empty((N, self.k), np.float32),
                    quality=np.empty((N, self.L), np.float32) if want_quality else None,
@@ -281,7 +288,7 @@ class Router:
 
     def argus_route_batch_dev(self, prompts_dev, quota, option, topk_idx, topk_score, quality=None,
                               status=None, N=None):
-        quota = np.ascontiguousarray(quota, np.int32)
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
         N = int(prompts_dev.shape[0]) if N is None else int(N)
         return _check(_lib.argus_route_batch_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
                                                  _p(topk_idx), _p(topk_score), _p(quality), _p(status)),
@@ -313,11 +320,12 @@ class Router:
                                                     _p(topk_idx), _p(topk_score), _p(quality), _p(status),
                                                     C.byref(ex)), "argus_route_batch_ex_dev")
 
-    def argus_route_batch_async(self, prompts, quota, out):
+    def argus_route_batch_async(self, prompts, quota, out, N=None):
         """Enqueue one batch from (pinned) host memory; outputs land in the arrays of
         `out` (option, topk_idx, topk_score, optional quality / status), which must
-        stay alive until argus_route_wait(ticket).  Returns the ticket."""
-        N = int(prompts.shape[0])
+        stay alive until argus_route_wait(ticket).  Returns the ticket.  Non-root
+        ranks of an NCCL router may pass prompts = None (and quota = None) with N."""
+        N = int(prompts.shape[0]) if prompts is not None else int(N)
         quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
         t = C.c_int64(-1)
         _check(_lib.argus_route_batch_async(self._h, _p(prompts), N, _p(quota), _p(out["option"]),

@@ -985,7 +985,8 @@ static int quota_ok(const argus_router* r, const int32_t* quota) {
 int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_t G, int32_t N,
                            const int32_t* quota, int32_t* option_out_dev, uint32_t* topk_idx_dev,
                            float* topk_score_dev, float* quality_dev, uint8_t* status_dev) {
-  if (G < 1 || !keys_all_dev) return ARGUS_E_INVALID;
+  // the tail stages G lists per prompt in shared memory sized for cfg.world at init
+  if (!r || G != r->cfg.world || !keys_all_dev || (reinterpret_cast<uintptr_t>(keys_all_dev) & 7)) return ARGUS_E_INVALID;
   return finish_impl(r, keys_all_dev, G, N, quota, option_out_dev, topk_idx_dev, topk_score_dev, quality_dev,
                      status_dev, r->stream, true);
 }
@@ -1008,6 +1009,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
   m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
   m.Xb = r->d_Xb[r->cur];  // the bf16 copy of this batch made by partial_impl
+  m.inv_q = r->d_invq[r->cur];
   m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;

@@ -23,6 +23,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                "l"(gmem)
                : "memory");
 }
+// 8-byte variant (LDGSTS.64, L1-allocating .ca: .cg takes 16-byte copies only) for
+// sources that are only 8-byte aligned.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Monotone map fp32 -> u32 (a < b  <=>  ord(a) < ord(b) for non-NaN a, b).

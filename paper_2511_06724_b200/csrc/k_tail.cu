@@ -323,13 +323,22 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   // block's keys (P slabs of 16 prompts x k, contiguous per list) arrive with one burst of
   // async copies; then one half-warp per prompt folds them from shared memory.
   uint64_t* kst = reinterpret_cast<uint64_t*>(ss + PB * 8);  // [P][PB][k]
-  {
+  // A list starts at (p * N + i0) * k keys: 16-byte aligned for every p only when N * k
+  // is even (and the buffer itself is); otherwise the keys move 8 bytes at a time.
+  if ((((a.N * k) & 1) | (int)(reinterpret_cast<uintptr_t>(a.keys_in) & 15)) == 0) {
     const int slab = PB * k / 2;  // 16-byte chunks per list
     for (int x = tid; x < a.P * slab; x += TT) {
       const int p = x / slab, c = x - p * slab;
       if (i0 * k + 2 * c < a.N * k)  // prompts past N: left unfilled, never read
         cp_async16(kst + (size_t)p * PB * k + 2 * c,
                    reinterpret_cast<const uint4*>(a.keys_in + ((int64_t)p * a.N + i0) * k) + c);
+    }
+  } else {
+    const int slab = PB * k;  // keys per list
+    for (int x = tid; x < a.P * slab; x += TT) {
+      const int p = x / slab, e = x - p * slab;
+      if (i0 * k + e < a.N * k)  // exactly the keys of prompts < N: nothing past the buffer
+        cp_async8(kst + (size_t)p * PB * k + e, a.keys_in + ((int64_t)p * a.N + i0) * k + e);
     }
   }
   cp_async_wait_all();
@@ -567,6 +576,9 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       }
     }
     if (lane == 0) {
+      // K6 flags a non-finite / zero-norm prompt only where it runs (the root); every
+      // rank sees the broadcast inv_q = 0 of that prompt, so every rank fails the call
+      if (__ldg(a.inv_q + i) == 0.f) atomicOr(a.flags, FLAG_INVALID_INPUT);
       a.ccount[i] = (uint8_t)__popc(cmask);
       a.cmask[i] = cmask;
       a.status[i] = st;

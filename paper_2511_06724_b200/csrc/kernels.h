@@ -106,6 +106,7 @@ struct TailArgs {
   uint64_t* topk_handle;     // [N][k] out or nullptr
   // predictor
   const __nv_bfloat16* Xb;   // [n_pad][d]
+  const float* inv_q;        // [n_pad] 0 marks an invalid prompt (K6 on the root; broadcast to every rank)
   const void* W1xF;          // W1x bf16 in mma.sync B-fragment order (see k_prep_w1_frag)
   const float* W1sT;         // [k][H]
   const float* b1;           // [H]

@@ -32,3 +32,46 @@ def test_product_bench_refuses_without_gpu():
     out = subprocess.run([sys.executable, "bench.py", "--config", "C1", "--steps", "1", "--warmup", "0"], cwd=ROOT,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode != 0
+
+
+def test_gpus_n_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as two ranks (torchrun,
+    127.0.0.1) which rendezvous; rank 0 alone prints the line (launcher check on CPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                           "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and sorted(j["ranks"]) == [0, 1] and j["max_over_ranks"] == 1.0
+
+
+def test_gpus_mismatch_refused():
+    """A WORLD_SIZE that disagrees with --gpus is an error, not a silent 1-GPU run."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=ROOT, env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode != 0
+
+
+def test_timed_schedule_represents_trace():
+    """Any K samples the bursty trace's low / high states in proportion (quantile
+    sample of the sizes, in trace order); K >= NT runs whole passes first."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import argus_inputs as gen
+    sizes = gen.bursty_sizes(256, seed=2018, lo=16, hi=512)
+    full = np.mean(sizes)
+    hi_frac = np.mean(np.asarray(sizes) > 256)
+    for K in (20, 30, 64, 100, 600):
+        sch = bench.timed_schedule(sizes, K)
+        assert len(sch) == K
+        ts = np.asarray([sizes[b] for b in sch])
+        assert abs(ts.mean() / full - 1) < 0.05, (K, ts.mean(), full)
+        assert abs(np.mean(ts > 256) - hi_frac) <= 1.0 / K + 0.02, K
+        rem = sch[(K // 256) * 256:]
+        assert rem == sorted(rem)   # trace order
+    assert bench.timed_schedule(sizes, 512) == list(range(256)) * 2

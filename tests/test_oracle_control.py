@@ -30,6 +30,38 @@ def test_uniform24_exact_and_in_range():
     assert oc.uniform24(7, 3, 5) != oc.uniform24(7, 4, 5) != oc.uniform24(8, 3, 5)
 
 
+def test_uniform24_golden_counter_layout(golden):
+    """R20's draw against cuRAND's independent Philox4x32-10 (tests/golden/pasm_uniform.json,
+    tools/gen_pasm_golden.cu): pins the counter layout {i, seq lo, seq hi, 0}, the key
+    {seed lo, seed hi}, the use of word x0 (not x1) and the >> 8 scaling.  Case 0 is also
+    the Random123 zero KAT: x0 = 0x6627e8d5."""
+    g = golden("pasm_uniform.json")["cases"]
+    assert g[0]["x0"] == "6627e8d5"
+    for c in g:
+        u = oc.uniform24(c["seed"], c["seq"], c["i"])
+        assert u.dtype == np.float32
+        assert float(u) == c["u_m"] / 16777216.0, c
+        assert c["u_m"] == hx(c["x0"]) >> 8
+        assert float(u) != (hx(c["x1"]) >> 8) / 16777216.0   # word x0, not x1
+
+
+def test_pasm_sample_strict_boundary(golden):
+    """u == cdf_j exactly selects j + 1 (a = first j with u < cdf_j, R20): the row
+    (u, 1 - u) for prompt 0 of call 0 under seed 0 must land on option 1."""
+    c = golden("pasm_uniform.json")["cases"][0]
+    u = np.float32(c["u_m"] / 16777216.0)
+    P = np.array([[float(u), 1.0 - float(u)], [0.0, 1.0]])
+    cdf = oc.pasm_cdf32(P)
+    assert cdf[0][0] == u
+    assert oc.pasm_sample(P[0], cdf[0], u) == 1
+    # one ulp (2^-24 steps are exact here) below the boundary stays on option 0
+    assert oc.pasm_sample(P[0], cdf[0], np.float32(u - np.float32(2 ** -24))) == 0
+    # the same through the per-batch sampler: o_0 = 0 (option 1 non-compliant)
+    opts = [dict(model_id=0, k_skip=0, p_th_qpm=10.0, sim_gate=0.0), dict(model_id=1, k_skip=0, p_th_qpm=20.0, sim_gate=0.0)]
+    res = oc.pasm_assign(np.array([[1.0, 0.5]]), np.array([0.3]), opts, P, 0, 0)
+    assert res["optimal"][0] == 0 and res["option"][0] == 1
+
+
 # ------------------------------------------------------------------ ODA (Alg. 1)
 def test_oda_spec_traces(golden):
     for c in golden("oda_spec.json")["cases"]:

@@ -52,6 +52,10 @@ def _load():
         lib.orc_cosine.argtypes = [P, P, C.c_int32]
         lib.orc_scan_topk.restype = C.c_int
         lib.orc_scan_topk.argtypes = [P, C.c_int32, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int, P, P]
+        lib.orc_score_matrix.restype = C.c_int
+        lib.orc_score_matrix.argtypes = [P, C.c_int32, P, C.c_int64, C.c_int32, C.c_int, P]
+        lib.orc_topk_of_scores.restype = C.c_int
+        lib.orc_topk_of_scores.argtypes = [P, C.c_int32, C.c_int64, C.c_int64, C.c_int32, P, P, P]
         lib.orc_mlp.restype = C.c_int
         lib.orc_mlp.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 P, P, P, P, C.c_int, P]
@@ -104,6 +108,34 @@ def scan_topk(X, Cache, k: int, ids=None, threads: int = 0):
     rc = _load().orc_scan_topk(_p(X), N, _p(Cache) if M else None, M, d, k, idp, threads, _p(sc), _p(ix))
     if rc != 0:
         raise ValueError("oracle scan: invalid input (zero norm or non-finite)")
+    return sc, ix
+
+
+def score_matrix(X, Cache, threads: int = 0) -> np.ndarray:
+    """O1..O3 for every pair: cos(x_i, c_j) f64 [N, M] (NaN for a zero-norm row)."""
+    X, Cache = _f32(X), _f32(Cache)
+    N, d = X.shape
+    M = Cache.shape[0]
+    S = np.empty((N, M), np.float64)
+    if N and M:
+        _load().orc_score_matrix(_p(X), N, _p(Cache), M, d, threads, _p(S))
+    return S
+
+
+def topk_of_scores(S, k: int, ids=None):
+    """O4 alone on a given score matrix S [N, M] (widened to fp64): the k best
+    (s desc, g asc) per row.  Parity test T2 replays it on the GPU's fp32 scores."""
+    S = np.ascontiguousarray(S, np.float64)
+    N, M = S.shape
+    sc = np.empty((N, k), np.float64)
+    ix = np.empty((N, k), np.uint32)
+    idp = None
+    if ids is not None:
+        ids = np.ascontiguousarray(ids, np.uint32)
+        idp = _p(ids)
+    rc = _load().orc_topk_of_scores(_p(S), N, M, M, k, idp, _p(sc), _p(ix))
+    if rc != 0:
+        raise ValueError("oracle topk: invalid shapes")
     return sc, ix
 
 

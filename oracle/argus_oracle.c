@@ -88,11 +88,35 @@ double orc_cosine(const float* x, const float* c, int32_t d) {
     return dot_bf16(x, c, d) / (nx * nc);
 }
 
+/* O3 for every pair: S[i][j] = cos(x_i, c_j) in fp64 over the bf16 values (the full
+ * N x M matrix, for element-wise parity of the GPU's captured scores, T1/T2). */
+int orc_score_matrix(const float* X, int32_t N, const float* C, int64_t M, int32_t d, int nthreads, double* S) {
+    if (N < 0 || M < 0 || d <= 0) return ORC_EINVAL;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int32_t i = 0; i < N; ++i)
+        for (int64_t j = 0; j < M; ++j) S[(int64_t)i * M + j] = orc_cosine(X + (int64_t)i * d, C + j * d, d);
+    return ORC_OK;
+}
+
 /* ---------------------------------------------------------------- O4: top-k */
 /* (s, g) beats (s', g') iff s > s' or (s == s' and g < g').  Ties go to the
  * older (lower-id) cache entry. */
 static int better(double s, uint32_t g, double s2, uint32_t g2) {
     return s > s2 || (s == s2 && g < g2);
+}
+
+/* O4 step: insert (s, g) into the sorted best-k list bs/bg holding *filled entries. */
+static void topk_insert(double s, uint32_t g, int32_t k, int* filled, double* bs, uint32_t* bg) {
+    if (*filled < k || better(s, g, bs[k - 1], bg[k - 1])) {
+        int p = *filled < k ? (*filled)++ : k - 1;
+        while (p > 0 && better(s, g, bs[p - 1], bg[p - 1])) {
+            bs[p] = bs[p - 1]; bg[p] = bg[p - 1]; --p;
+        }
+        bs[p] = s; bg[p] = g;
+    }
 }
 
 /* For each prompt: the k best (s, g) over all cache rows, sorted best first.
@@ -145,18 +169,28 @@ int orc_scan_topk(const float* X, int32_t N, const float* C, int64_t M, int32_t 
             for (int32_t l = 0; l < d; ++l) dot += (double)x[l] * (double)c[l];
             double s = dot / (nx * nc[j]);                           /* O3 */
             uint32_t g = ids ? ids[j] : (uint32_t)j;
-            /* O4: insert (s, g) into the sorted best-k list */
-            if (filled < k || better(s, g, bs[k - 1], bg[k - 1])) {
-                int p = filled < k ? filled++ : k - 1;
-                while (p > 0 && better(s, g, bs[p - 1], bg[p - 1])) {
-                    bs[p] = bs[p - 1]; bg[p] = bg[p - 1]; --p;
-                }
-                bs[p] = s; bg[p] = g;
-            }
+            topk_insert(s, g, k, &filled, bs, bg);                  /* O4 */
         }
     }
     free(Cb); free(Xb); free(nc);
     return badq ? ORC_EINVAL : ORC_OK;
+}
+
+/* O4 alone on given scores S [N][M] (row stride ld; parity test T2 replays it on
+ * the GPU's own fp32 scores): the k best (s, g) per row, sorted
+ * best first, padded like orc_scan_topk.  ids[j] is the global id of column j. */
+int orc_topk_of_scores(const double* S, int32_t N, int64_t M, int64_t ld, int32_t k, const uint32_t* ids,
+                       double* topk_score, uint32_t* topk_idx) {
+    if (N < 0 || M < 0 || ld < M || k <= 0) return ORC_EINVAL;
+    for (int32_t i = 0; i < N; ++i) {
+        double* bs = topk_score + (int64_t)i * k;
+        uint32_t* bg = topk_idx + (int64_t)i * k;
+        for (int32_t t = 0; t < k; ++t) { bs[t] = -1.0; bg[t] = 0xFFFFFFFFu; }
+        int filled = 0;
+        for (int64_t j = 0; j < M; ++j)
+            topk_insert(S[(int64_t)i * ld + j], ids ? ids[j] : (uint32_t)j, k, &filled, bs, bg);
+    }
+    return ORC_OK;
 }
 
 /* ---------------------------------------------------------------- O5: predictor */

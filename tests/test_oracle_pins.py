@@ -139,6 +139,43 @@ def test_topk_permutation_relabels():
     np.testing.assert_array_equal(s0, s1)
 
 
+def test_topk_of_scores_brute_force():
+    """O4 alone (the T2 replay): np.lexsort by (-s, id) on scores with many exact ties
+    (two-decimal values), -0.0 tying with +0.0 by id, ids relabelling, k > M padding."""
+    rng = np.random.default_rng(44)
+    for trial in range(40):
+        N, M = int(rng.integers(1, 6)), int(rng.integers(0, 40))
+        k = int(rng.integers(1, 9))
+        S = np.round(rng.uniform(-1, 1, (N, M)), 1 + trial % 2)
+        if M > 3:
+            S[:, 1], S[:, 3] = -0.0, 0.0   # lower id holds -0.0: must still come first
+        ids = rng.permutation(1000)[:M].astype(np.uint32) if trial % 3 == 0 else None
+        sc, ix = oracle.topk_of_scores(S, k, ids=ids)
+        g = np.arange(M) if ids is None else ids.astype(np.int64)
+        for i in range(N):
+            order = np.lexsort((g, -S[i]))[:k]
+            n = min(k, M)
+            assert list(ix[i, :n]) == [int(g[j]) for j in order], (trial, i)
+            assert list(sc[i, :n]) == [float(S[i, j]) for j in order]
+            assert list(ix[i, n:]) == [0xFFFFFFFF] * (k - n) and list(sc[i, n:]) == [-1.0] * (k - n)
+
+
+def test_topk_of_scores_agrees_with_scan():
+    """The scan's O4 and the standalone O4 agree on the oracle's own cosines."""
+    rng = np.random.default_rng(45)
+    Cc = rng.standard_normal((70, 16)).astype(np.float32)
+    Cc[30] = Cc[7]
+    X = rng.standard_normal((4, 16)).astype(np.float32)
+    X[0] = Cc[7]
+    S = np.array([[oracle.cosine(x, c) for c in Cc] for x in X])
+    np.testing.assert_array_equal(oracle.score_matrix(X, Cc), S)
+    s0, i0 = oracle.scan_topk(X, Cc, 6)
+    s1, i1 = oracle.topk_of_scores(S, 6)
+    np.testing.assert_array_equal(i0, i1)
+    np.testing.assert_array_equal(s0, s1)
+    assert list(i0[0, :2]) == [7, 30]
+
+
 def test_topk_rejects_zero_norm():
     with pytest.raises(ValueError):
         oracle.scan_topk(np.zeros((1, 8), np.float32), np.ones((2, 8), np.float32), 1)

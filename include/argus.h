@@ -383,6 +383,19 @@ int argus_get_stream(const argus_router* r, void** stream_out);
 int argus_profile_enable(argus_router* r, int on);
 int argus_profile_read(argus_router* r, int stage, double* total_ms, int64_t* launches);
 
+/* Score capture for parity test T2 (SURVEY §8(c).iii "oracle O4 on the GPU's fp32
+ * scores equals the GPU's top-k exactly, including order"); debug sizes only.
+ * While scores_dev != NULL, the scan of every later route call also writes each
+ * score its fused top-k compares -- S[i][j] = fl32(fl32(acc_ij * inv_c[j]) * inv_q[i]),
+ * acc the tensor-core fp32 dot product of the bf16 rows (P:132 cosine similarity) --
+ * to scores_dev[i * ld + j] for prompts i < N and this shard's local slots j < its
+ * live rows (slot j holds cache position j * world + rank).  scores_dev is device
+ * fp32 owned by the caller and must stay allocated until capture is switched off
+ * (scores_dev = NULL); entries of other slots are left untouched.  A route call
+ * whose shard has more live rows than ld fails with ARGUS_E_INVALID.  Costs an
+ * N x M write per batch: a test setting, never a production one. */
+int argus_debug_capture(argus_router* r, float* scores_dev, int64_t ld);
+
 /* Free all device memory, the NCCL communicator and the router. */
 int argus_route_destroy(argus_router* r);
 

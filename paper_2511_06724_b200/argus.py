@@ -35,6 +35,7 @@ SYMBOLS = (
     "argus_strerror", "argus_solve_allocation", "argus_oda_pasm", "argus_pasm_degradation", "argus_set_policy",
     "argus_affinity_histogram", "argus_set_workers", "argus_get_queues", "argus_route_batch_ex",
     "argus_route_batch_ex_dev", "argus_cache_insert_h", "argus_route_batch_async", "argus_route_wait",
+    "argus_debug_capture",
 )
 STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
@@ -99,6 +100,7 @@ def _load():
         "argus_cache_insert_h": [P, P, P, I64, P],
         "argus_route_batch_async": [P, P, I32, P, P, P, P, P, P, P],
         "argus_route_wait": [P, I64],
+        "argus_debug_capture": [P, P, I64],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -384,6 +386,17 @@ class Router:
         return _check(_lib.argus_route_finish_dev(self._h, _p(keys_all_dev), int(G), int(N), _p(quota),
                                                   _p(option), _p(topk_idx), _p(topk_score), _p(quality),
                                                   _p(status)), "argus_route_finish_dev")
+
+    def argus_debug_capture(self, scores_dev=None, ld=None):
+        """Parity test T2: later scans also write every exact score they compare into
+        scores_dev (device fp32 [N][ld], ld >= this shard's live rows); None switches off."""
+        if scores_dev is None:
+            _check(_lib.argus_debug_capture(self._h, None, 0), "argus_debug_capture")
+            self._dbg_keep = None
+            return
+        ld = int(scores_dev.shape[-1]) if ld is None else int(ld)
+        self._dbg_keep = scores_dev
+        _check(_lib.argus_debug_capture(self._h, _p(scores_dev), ld), "argus_debug_capture")
 
     def argus_profile_enable(self, on=True):
         _check(_lib.argus_profile_enable(self._h, int(bool(on))), "argus_profile_enable")

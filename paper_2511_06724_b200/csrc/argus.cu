@@ -186,6 +186,9 @@ struct argus_router {
   int scan_reserve = 2;            // pipelined one-slice scans: SMs left to prep / tail (ARGUS_SCAN_RESERVE)
   bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
+  // argus_debug_capture (parity test T2): the scan also writes every exact score here
+  float* dbg_scores = nullptr;
+  int64_t dbg_ld = 0;
   // stage profiling (argus_profile_*)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -333,6 +336,13 @@ static void prof_collect(argus_router* r) {
 
 // ------------------------------------------------------------------ C ABI
 extern "C" {
+
+int argus_debug_capture(argus_router* r, float* scores_dev, int64_t ld) {
+  if (!r || (scores_dev && ld < 1)) return ARGUS_E_INVALID;
+  r->dbg_scores = scores_dev;
+  r->dbg_ld = scores_dev ? ld : 0;
+  return ARGUS_OK;
+}
 
 int argus_profile_enable(argus_router* r, int on) {
   if (!r) return ARGUS_E_INVALID;
@@ -905,6 +915,9 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.rank = r->cfg.rank;
   a.world = r->cfg.world;
   a.partial = r->d_partial[q];
+  a.dbg = r->dbg_scores;
+  a.dbg_ld = r->dbg_ld;
+  if (a.dbg && a.dbg_ld < a.m_local) return ARGUS_E_INVALID;  // capture rows too short for the shard
   a.gthr = r->d_gthr[q];
   a.ctr = r->d_ctr[q];
   bool pair = r->pair_scan && scan_pair_supported(d, N);

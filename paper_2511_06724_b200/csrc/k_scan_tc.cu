@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t icp = tc::smem_u32(&sm->invc[l & (INV_SLOTS - 1)][h * 32]);
         const int64_t rem_rows = a.m_local - j0;
         const int cmax = rem_rows < 32 ? (rem_rows < 0 ? 0 : (int)rem_rows) : 32;
+        if (a.dbg != nullptr && active) epi_dump(v, icp, iq, cmax, a.dbg + (int64_t)p * a.dbg_ld + j0);
         epi_chunk<KMAX>(v, icp, iq, cmax, (uint32_t)(j0 * a.world + a.rank), (uint32_t)a.world, a.head, a.capg, tl,
                         thr, scratch);
         // publish only a local bound that beats everything seen so far (rare after warm-up)

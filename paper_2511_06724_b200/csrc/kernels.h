@@ -52,6 +52,8 @@ struct ScanArgs {
   int32_t home_max;          // pair scan: home pairs per pair slice = their list slots [0, home_max)
   int32_t floaters;          // pair scan: pairs beyond home_max * pair slices (slots home_max + f)
   int32_t grid_ctas;         // pair scan with migration: CTAs launched (all SMs' pairs)
+  float* dbg;                // argus_debug_capture: every exact score to dbg[p * dbg_ld + slot] (NULL: off)
+  int64_t dbg_ld;
 };
 constexpr int MAX_SLICES = 64;  // max_batch <= 8192 = 64 slices of 128 prompts
 constexpr int CTR_WORDS = 3 * MAX_SLICES;

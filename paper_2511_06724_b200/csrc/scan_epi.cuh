@@ -82,4 +82,13 @@ __device__ __forceinline__ void epi_chunk(uint32_t (&v)[32], uint32_t icp, float
   }
 }
 
+// argus_debug_capture (parity test T2): the chunk's exact scores, computed exactly as
+// epi_chunk computes them (fl(fl(acc * inv_c) * inv_q)), to row[c] for c < cmax.  Must
+// run before epi_chunk, which overwrites v with the scaled values.
+__device__ __forceinline__ void epi_dump(const uint32_t (&v)[32], uint32_t icp, float iq, int cmax, float* row) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c)  // unrolled: v stays in registers
+    if (c < cmax) row[c] = __fmul_rn(__fmul_rn(__uint_as_float(v[c]), tc::lds_f32(icp + c * 4)), iq);
+}
+
 }  // namespace argus

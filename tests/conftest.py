@@ -29,3 +29,18 @@ def golden():
         with open(os.path.join(ROOT, "tests", "golden", name)) as f:
             return json.load(f)
     return load
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Parity statistics gathered by tests/parity.py (T3 exemption rates, A2 matched
+    prefixes, T2 exact replays), one line per check."""
+    try:
+        from tests import parity
+    except Exception:
+        return
+    if not parity.REPORT:
+        return
+    tr = terminalreporter
+    tr.section("parity report (SURVEY §8(c).iii)")
+    for rec in parity.REPORT:
+        tr.write_line(" ".join(f"{k}={v}" for k, v in rec.items()))

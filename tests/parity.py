@@ -7,6 +7,9 @@ the oracle's score gap at the boundary is below 1e-3".
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import oracle
@@ -14,6 +17,21 @@ import oracle
 SCORE_TOL = 2e-2    # T1, M1, M2
 GAP_TOL = 1e-3      # T3 boundary-gap exemption, A2 fragility
 DELTA32 = float(np.float32(oracle.DELTA))
+
+# Per-test parity statistics (T3 exemption rates, A2 matched-prefix fractions, T2
+# replays), printed at the end of the session by tests/conftest.py and written to
+# $ARGUS_PARITY_REPORT (JSON lines) when that is set.
+REPORT = []
+
+
+def report(kind, **kw):
+    rec = dict(test=os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], kind=kind, **kw)
+    REPORT.append(rec)
+    path = os.environ.get("ARGUS_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    return rec
 
 
 def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
@@ -77,7 +95,22 @@ def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
         # order: GPU list sorted by its own scores, descending (ties -> lower id)
         for t in range(nreal - 1):
             assert (gs[t] > gs[t + 1]) or (gs[t] == gs[t + 1] and gi[t] < gi[t + 1]), (i, gs, gi)
-    return dict(exempt_rows=exempt, max_score_err=max_err, rows=len(list(rows)))
+    nrows = len(list(rows))
+    report("T3", rows=nrows, exempt_rows=exempt, exempt_rate=round(exempt / max(1, nrows), 4), M=int(M), k=int(k),
+           max_score_err=max_err)
+    return dict(exempt_rows=exempt, max_score_err=max_err, rows=nrows)
+
+
+def check_topk_replay(S_gpu, gpu_idx, gpu_score, k, ids=None):
+    """T2: oracle O4 run on the GPU's own fp32 scores (S_gpu [N, M], captured from the
+    scan by argus_debug_capture) must give the GPU's top-k exactly -- ids, scores and
+    order.  This checks the fused filter / top-k / merges independently of rounding."""
+    S_gpu = np.asarray(S_gpu, np.float32)
+    assert np.isfinite(S_gpu).all(), "capture left unwritten (NaN) entries"
+    sc, ix = oracle.topk_of_scores(S_gpu.astype(np.float64), k, ids=ids)
+    np.testing.assert_array_equal(np.asarray(gpu_idx, np.uint32), ix)
+    np.testing.assert_array_equal(np.asarray(gpu_score, np.float32).astype(np.float64), sc)
+    report("T2", rows=int(S_gpu.shape[0]), M=int(S_gpu.shape[1]), k=int(k), exact=True)
 
 
 def check_replay(gpu, opts, quota, delta=oracle.DELTA):
@@ -147,4 +180,47 @@ def check_e2e(ores, gpu, opts, quota):
     if exempt == 0:
         np.testing.assert_array_equal(gpu["option"], ores["option"])
         np.testing.assert_array_equal(gpu["status"], ores["status"])
+    prefix = matched_prefix(ores, rep, gpu, opts, quota)
+    report("A2", prompts=int(N), exempt=int(exempt), matched_prefix=prefix,
+           matched_prefix_frac=round(prefix / max(1, N), 4))
     return exempt
+
+
+def fragile_mask(ores, opts, quota):
+    """prompt i is fragile when, in the oracle's fp64 values,
+    min(min_{v>=1} |r_iv - delta|, min_{v gated} |s_i1 - tau_v|,
+        min_{v in A_i free at its turn, v != a_i} |r_{i,a_i} - r_iv|) < GAP_TOL,
+    with "free at its turn" replayed along the oracle's priority order."""
+    r, s1 = ores["rhat"], ores["topk_score"][:, 0]
+    N, L = r.shape
+    rem = np.array(quota, np.int64).copy()
+    frag = np.zeros(N, bool)
+    for i in ores["order"]:
+        a = int(ores["option"][i])
+        m = min([abs(r[i, v] - DELTA32) for v in range(1, L)] or [1.0])
+        for v in range(L):
+            if opts[v]["k_skip"] != 0:
+                m = min(m, abs(s1[i] - float(np.float32(opts[v]["sim_gate"]))))
+            if v != a and (ores["adm"][i] >> v) & 1 and rem[v] > 0:
+                m = min(m, abs(r[i, a] - r[i, v]))
+        frag[i] = m < GAP_TOL
+        if not (ores["status"][i] & oracle.OVERFLOW):
+            rem[a] -= 1
+    return frag
+
+
+def matched_prefix(ores, rep, gpu, opts, quota):
+    """A2 matched prefix: the longest prefix of the oracle's priority order that (a)
+    the GPU's own priority order (replayed from its fp32 values) shares and (b)
+    holds no fragile prompt.  Along it both serial dictatorships see the same
+    prompts with the same preference lists and quotas, so every assignment and
+    status there must be identical (asserted).  Returns its length."""
+    frag = fragile_mask(ores, opts, quota)
+    oo, go = np.asarray(ores["order"]), np.asarray(rep["order"])
+    t = 0
+    while t < len(oo) and oo[t] == go[t] and not frag[oo[t]]:
+        t += 1
+    idx = oo[:t]
+    np.testing.assert_array_equal(gpu["option"][idx], ores["option"][idx])
+    np.testing.assert_array_equal(gpu["status"][idx], ores["status"][idx])
+    return int(t)

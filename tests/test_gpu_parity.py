@@ -60,7 +60,10 @@ def test_c1_parity(argus_mod):
 
 
 @pytest.mark.parametrize("N,M,k,seed", [(77, 4133, 4, 11), (1, 300, 4, 12), (200, 9000, 8, 13),
-                                        (129, 2048 + 63, 2, 14), (300, 5000, 1, 15)])
+                                        (129, 2048 + 63, 2, 14), (300, 5000, 1, 15),
+                                        # odd N * k: candidate lists start 8 bytes off a 16-byte line
+                                        (77, 4133, 3, 16), (33, 9000, 7, 17), (75, 9000, 1, 18),
+                                        (257, 20000, 5, 19)])
 def test_ragged_parity(argus_mod, N, M, k, seed):
     p = gen.small_problem("C1", N=N, M=M, k=k, seed=seed)
     run_case(argus_mod, p)
@@ -148,7 +151,7 @@ def test_determinism(argus_mod):
 
 @pytest.mark.parametrize("N", [70, 256])
 def test_g_invariance_striped_shards(argus_mod, N):
-    """Outputs are bit-identical for G = 1, 2, 4 striped shards:
+    """Outputs are bit-identical for G = 1, 2, 3, 4, 8 striped shards:
     G routers on one GPU in external-collective mode, keys concatenated here.
     N = 256 runs the CTA-pair scan on every shard."""
     import torch
@@ -158,7 +161,7 @@ def test_g_invariance_striped_shards(argus_mod, N):
     quota = oracle.quota_from_fractions(p.fractions, N)
     X = torch.from_numpy(p.X).cuda()
     ref = None
-    for G in (1, 2, 4):
+    for G in (1, 2, 3, 4, 8):
         routers = [make_router(argus, p, rank=rk, world=G) for rk in range(G)]
         for r in routers:
             r.argus_cache_insert(p.cache)

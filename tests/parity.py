@@ -181,8 +181,9 @@ def check_e2e(ores, gpu, opts, quota):
         np.testing.assert_array_equal(gpu["option"], ores["option"])
         np.testing.assert_array_equal(gpu["status"], ores["status"])
     prefix = matched_prefix(ores, rep, gpu, opts, quota)
+    full = bool(np.array_equal(gpu["option"], ores["option"]) and np.array_equal(gpu["status"], ores["status"]))
     report("A2", prompts=int(N), exempt=int(exempt), matched_prefix=prefix,
-           matched_prefix_frac=round(prefix / max(1, N), 4))
+           matched_prefix_frac=round(prefix / max(1, N), 4), all_assignments_equal=full)
     return exempt
 
 

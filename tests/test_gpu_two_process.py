@@ -61,11 +61,16 @@ def _rank_main(rank, world, port, out_dir):
                 # a NaN prompt: the call fails on this rank too
                 bad = X.clone()
                 bad[3, 7] = float("nan")
+                def code(f):
+                    try:
+                        return f()
+                    except argus.ArgusError as e:
+                        return e.code
                 r.argus_route_partial_dev(bad, keys)
-                rcb = r.argus_sync()
+                rcb = code(r.argus_sync)
                 r.argus_route_finish_dev(keys_all, world, N, quota, o["option"], o["topk_idx"], o["topk_score"],
                                          o["quality"], o["status"])
-                res[N]["rc_nan"] = min(rcb, r.argus_sync())
+                res[N]["rc_nan"] = min(rcb, code(r.argus_sync))
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), res, allow_pickle=True)
     finally:
         dist.destroy_process_group()

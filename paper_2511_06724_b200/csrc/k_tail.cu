@@ -29,12 +29,22 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc.cuh"
 
 #ifndef ARGUS_TAIL_TIMING
 #define ARGUS_TAIL_TIMING 0  // diagnostics build only: device printf of phase timestamps
 #endif
 
 namespace argus {
+
+// diagnostics build: thread 0 stamps %globaltimer into shared memory at phase boundaries
+// (no registers held across the phases, so the instrumented kernel keeps the product's
+// register allocation); the launch's last CTA prints them
+__shared__ unsigned long long tail_ts[24];  // 20: clock64 at entry
+#define TS(i)                                                   \
+  do {                                                          \
+    if (ARGUS_TAIL_TIMING && threadIdx.x == 0) tail_ts[i] = gtimer(); \
+  } while (0)
 
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
@@ -65,19 +75,43 @@ __device__ __forceinline__ uint64_t half_max_u64(uint64_t x) {  // max over the 
   return x;
 }
 
-static size_t phase1_bytes(int d, int k, int P_max) {
-  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)TW * PB * 32 + (size_t)PB * 8) +
-         sizeof(uint64_t) * (size_t)P_max * PB * k;
+// Shared-memory layout of phases M / 1: [xs: PB x (d + 8) bf16][red: TW x PB x 32 f32][ss: PB x 8 f32]
+// [kst: P x PB x k u64].  Phase 2: [hs: PB x H f32] at 0 and W2 (rows padded to H + 4) at
+// w2_off = max(kst offset, PB H 4): the kst area is dead once the lists are merged, so W2 is
+// prefetched there during phase 1 and never collides with hs.
+__host__ __device__ __forceinline__ size_t kst_offset(int d) {
+  return (size_t)PB * (d + 8) * 2 + sizeof(float) * ((size_t)TW * PB * 32 + (size_t)PB * 8);
 }
-static size_t phase2_bytes(int H, int L) { return sizeof(float) * ((size_t)PB * H + (size_t)L * (H + 4)); }
+__host__ __device__ __forceinline__ size_t w2_offset(int d, int H) {
+  const size_t a = kst_offset(d), b = sizeof(float) * (size_t)PB * H;
+  return a > b ? a : b;
+}
+// Staged candidate lists are list-major with a padded list stride of S(k) keys: a list's
+// 16 prompts x k keys plus k pad keys (17 k, rounded up to even so every list starts on a
+// 16-byte boundary for the bulk copies).  With k | 16 the 16 / k lists a half-warp reads
+// at once then start k keys apart modulo 16 keys (32 banks): conflict-free.
+__host__ __device__ __forceinline__ int list_stride(int k) { return 17 * k + (k & 1); }
+static size_t phase1_bytes(int d, int k, int P_max) {
+  return kst_offset(d) + sizeof(uint64_t) * (size_t)P_max * list_stride(k);
+}
+static size_t phase2_bytes(int d, int H, int L) {
+  return w2_offset(d, H) + sizeof(float) * ((size_t)L * (H + 4) + (size_t)TW * (PB / TW) * 32 + 32);  // W2 | r | p_th
+}
+// Phase 3 layout: [order: N i32][cc: N u8, padded to 16][rk: CH x Lw u8][cm: CH u32][st: CH u8][opt: CH u8]
+// [inv: 32 x 32 u8, the SD warp's per-lane inverse of pi].
+// With N <= CH ("by index") rk / cm / st hold every prompt's row at its index, staged in the
+// same round trip as |C_i|; larger batches stage rows chunk by chunk in priority order.
+__host__ __device__ __forceinline__ size_t p3_rk_offset(int N) {
+  return sizeof(int32_t) * (size_t)N + (((size_t)N + 15) & ~(size_t)15);
+}
 static size_t phase3_bytes(int N, int L) {
   const int Lw = (L + 3) / 4 * 4;
-  return sizeof(int32_t) * (size_t)N + (size_t)CH * Lw + sizeof(uint32_t) * CH + CH;
+  return p3_rk_offset(N) + (size_t)CH * Lw + sizeof(uint32_t) * CH + 2 * (size_t)CH + 32 * 32;
 }
 
 size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max) {
   size_t b = phase1_bytes(d, k, P_max);
-  b = b > phase2_bytes(H, L) ? b : phase2_bytes(H, L);
+  b = b > phase2_bytes(d, H, L) ? b : phase2_bytes(d, H, L);
   b = b > phase3_bytes(max_batch, L) ? b : phase3_bytes(max_batch, L);
   return b;
 }
@@ -85,25 +119,53 @@ size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max) {
 // ------------------------------------------------------------------ phase 3
 __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
   const int N = a.N, L = a.L, Lw = a.Lw;
-  int32_t* order_s = reinterpret_cast<int32_t*>(smraw);                  // [N]
-  uint8_t* rk_s = smraw + sizeof(int32_t) * (size_t)N;                   // [CH][Lw]
-  uint32_t* cm_s = reinterpret_cast<uint32_t*>(rk_s + (size_t)CH * Lw);  // [CH]
-  uint8_t* opt_s = reinterpret_cast<uint8_t*>(cm_s + CH);                 // [CH] (option | 0x80 overflow)
+  const bool byidx = N <= CH;
+  int32_t* order_s = reinterpret_cast<int32_t*>(smraw);                   // [N]
+  uint8_t* cc_s = smraw + sizeof(int32_t) * (size_t)N;                    // [N]
+  uint8_t* rk_s = smraw + p3_rk_offset(N);                                 // [CH][Lw]
+  uint32_t* cm_s = reinterpret_cast<uint32_t*>(rk_s + (size_t)CH * Lw);   // [CH]
+  uint8_t* st_s = reinterpret_cast<uint8_t*>(cm_s + CH);                   // [CH]
+  uint8_t* opt_s = st_s + CH;                                              // [CH] (option | 0x80 overflow)
   __shared__ int32_t base[NB];
   __shared__ int32_t tot[NB];
   __shared__ int32_t wcnt[TW][NB];
+  __shared__ int32_t rem_s[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.prefl);
+  const int W = Lw / 4;
+  TS(12);
 
-  // stable counting sort of prompts by |C_i|
+  // one round trip: |C_i| of every prompt (and, by index, its mask, pi_i and status),
+  // then a warp-aggregated histogram of |C_i|
   if (tid < NB) base[tid] = 0;
+  if (tid < 32) {
+    int c = tid < L ? (a.quota_dev ? a.quota_dev[tid] : a.quota[tid]) : 0;
+    if (c < 0) {  // only reachable through the broadcast (the host API checks its own argument)
+      atomicOr(a.flags, FLAG_INVALID_INPUT);
+      c = 0;
+    }
+    rem_s[tid] = c;
+  }
   __syncthreads();
-  for (int i0 = 0; i0 < N; i0 += TT) {  // warp-aggregated histogram
+  for (int i0 = 0; i0 < N; i0 += TT) {
     const int i = i0 + tid;
     const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
+    if (byidx && i < N) {
+      cm_s[i] = __ldcg(a.cmask + i);
+      st_s[i] = __ldcg(a.status + i);
+      uint32_t wd[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) wd[w] = w < W ? __ldcg(rk32 + (int64_t)i * W + w) : 0u;
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)i * Lw)[w] = wd[w];
+    }
+    if (i < N) cc_s[i] = (uint8_t)b;
     const uint32_t peers = __match_any_sync(0xffffffffu, b);
     if (b >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&base[b], __popc(peers));
   }
   __syncthreads();
+  TS(13);
   if (warp == 0) {  // exclusive scan of the 33 bucket counts
     const int c0 = base[lane];
     int x = c0;
@@ -117,9 +179,9 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
     if (lane == 0) base[32] = tot31;
   }
   __syncthreads();
-  for (int c0 = 0; c0 < N; c0 += TT) {
+  for (int c0 = 0; c0 < N; c0 += TT) {  // stable scatter into priority order
     const int i = c0 + tid;
-    const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
+    const int b = i < N ? (int)cc_s[i] : -1;
     for (int x = tid; x < TW * NB; x += TT) (&wcnt[0][0])[x] = 0;
     __syncthreads();
     const uint32_t peers = __match_any_sync(0xffffffffu, b);
@@ -139,101 +201,133 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
   }
   __syncthreads();
 
-  // serial dictatorship over staged chunks
-  __shared__ int32_t rem_s[32];
-  if (tid < 32) {
-    int c = tid < L ? (a.quota_dev ? a.quota_dev[tid] : a.quota[tid]) : 0;
-    if (c < 0) {  // only reachable through the broadcast (the host API checks its own argument)
-      atomicOr(a.flags, FLAG_INVALID_INPUT);
-      c = 0;
-    }
-    rem_s[tid] = c;
-  }
+  // serial dictatorship over chunks of the priority order
+  TS(14);
   bool any_overflow = false;
-  const int W = Lw / 4;
-  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.prefl);
+  int rem_r = rem_s[lane];                                          // warp 0: lane v holds rem_v
+  if (ARGUS_TAIL_TIMING && tid == 0) tail_ts[22] = 0;
+  uint32_t avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
   for (int c0 = 0; c0 < N; c0 += CH) {
     const int n = min(CH, N - c0);
-    for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
-      int ii[4];
+    if (!byidx) {
+      for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
+        int ii[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = t0 + u * TT;
-        ii[u] = t < n ? order_s[c0 + t] : -1;
-      }
-      uint32_t cm[4];
-      uint32_t wd[4][8];
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * TT;
+          ii[u] = t < n ? order_s[c0 + t] : -1;
+        }
+        uint32_t cm[4];
+        uint8_t st[4];
+        uint32_t wd[4][8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        cm[u] = ii[u] >= 0 ? __ldcg(a.cmask + ii[u]) : 0u;
+        for (int u = 0; u < 4; ++u) {
+          cm[u] = ii[u] >= 0 ? __ldcg(a.cmask + ii[u]) : 0u;
+          st[u] = ii[u] >= 0 ? __ldcg(a.status + ii[u]) : (uint8_t)0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) wd[u][w] = (ii[u] >= 0 && w < W) ? __ldcg(rk32 + (int64_t)ii[u] * W + w) : 0u;
-      }
+          for (int w = 0; w < 8; ++w) wd[u][w] = (ii[u] >= 0 && w < W) ? __ldcg(rk32 + (int64_t)ii[u] * W + w) : 0u;
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int t = t0 + u * TT;
-        if (t < n) {
-          cm_s[t] = cm[u];
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * TT;
+          if (t < n) {
+            cm_s[t] = cm[u];
+            st_s[t] = st[u];
 #pragma unroll
-          for (int w = 0; w < 8; ++w)
-            if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = wd[u][w];
+            for (int w = 0; w < 8; ++w)
+              if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = wd[u][w];
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (warp == 0) {
-      // Serial dictatorship, 32 prompts at a time.  Each lane takes the first option of
-      // its pi_i that had quota left when the group started; the group's choices are
-      // exactly the sequential ones up to the first lane whose option was used up by
-      // earlier lanes of the group (running count >= remaining quota).  Those lanes
-      // commit, the rest restart with the new quotas.  An option runs out at most once,
-      // so a batch takes at most N/32 + L group steps.
-      uint32_t avail = __ballot_sync(0xffffffffu, lane < L && rem_s[lane] > 0);
+      // Serial dictatorship over a window of 32 prompts in priority order (lane = rank in
+      // the window), lane v holding rem_v.  Every pending lane takes the first option of
+      // its pi with quota left; the choices equal the sequential ones up to the first
+      // pending lane whose option earlier pending lanes used up (their count >= rem).
+      // Those lanes commit and the rest retry with the new quotas.  An option runs out at
+      // most once, so a window takes at most 1 + L steps.  A step is a handful of votes:
+      // each lane keeps the ranks (positions in its pi) still available as a bit mask A,
+      // clears the rank of each option that ran out (looked up in a per-lane inverse of
+      // pi in shared memory) and reads its choice at the lowest remaining rank.
+      uint8_t* inv = opt_s + CH + lane * 32;  // [32 lanes][32 options] rank of option v in pi, 0xFF if absent
 #pragma unroll 1
-      for (int t = 0; t < n;) {
-        const int j = t + lane;
-        int choice = 0xFF;  // no admissible option with quota left: overflow
-        if (j < n) {
-          const uint8_t* row = rk_s + (size_t)j * Lw;
-#pragma unroll 1
-          for (int r = 0; r < Lw; ++r) {
-            const int o = row[r];
-            if (o == 0xFF) break;
-            if ((avail >> o) & 1u) {
-              choice = o;
-              break;
+      for (int t0 = 0; t0 < n; t0 += 32) {
+        const int jj = t0 + lane;
+        const bool act = jj < n;
+        const uint8_t* row = rk_s + (size_t)(act ? (byidx ? order_s[jj] : jj) : 0) * Lw;
+        uint32_t A = 0;  // ranks whose option has quota left
+        if (act) {
+          const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
+          for (int q = 0; q < 8; ++q) reinterpret_cast<uint32_t*>(inv)[q] = 0xFFFFFFFFu;
+          for (int q = 0; q < W; ++q) {
+            const uint32_t wq = row32[q];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const uint32_t o = (wq >> (8 * b)) & 0xFFu;
+              if (o != 0xFFu) {
+                inv[o] = (uint8_t)(4 * q + b);
+                if ((avail_r >> o) & 1u) A |= 1u << (4 * q + b);
+              }
             }
           }
         }
-        const uint32_t peers = __match_any_sync(0xffffffffu, choice);
-        const int before = __popc(peers & ((1u << lane) - 1u));
-        const bool ok = j >= n || choice == 0xFF || before < rem_s[choice];
-        const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
-        const int take = min(bad ? __ffs(bad) - 1 : 32, n - t);  // >= 1: lane 0 is always ok
         __syncwarp();
-        if (lane < take) {
-          opt_s[j] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
-          if (choice != 0xFF) atomicSub(&rem_s[choice], 1);
-          any_overflow |= choice == 0xFF;
+        uint32_t pending = __ballot_sync(0xffffffffu, act);
+        const uint32_t lt = (1u << lane) - 1u;
+        uint32_t seen = avail_r;  // options whose exhaustion A already reflects
+#pragma unroll 1
+        while (pending) {
+          for (uint32_t ex = seen & ~avail_r; ex; ex &= ex - 1) {  // options that ran out
+            const uint32_t r = inv[__ffs(ex) - 1];
+            if (r != 0xFFu) A &= ~(1u << r);
+          }
+          seen = avail_r;
+          const bool mine = (pending >> lane) & 1u;
+          const int choice = A ? (int)row[__ffs(A) - 1] : 0xFF;  // 0xFF: no quota left, overflow
+          // lanes with the same choice from five bit-ballots
+          const bool real = mine && choice != 0xFF;
+          const uint32_t V = __ballot_sync(0xffffffffu, real);
+          uint32_t same = V, mv = V;  // lanes choosing my option / choosing option `lane`
+#pragma unroll
+          for (int b = 0; b < 5; ++b) {
+            const uint32_t B = __ballot_sync(0xffffffffu, real && ((choice >> b) & 1));
+            same &= ((choice >> b) & 1) ? B : ~B;
+            mv &= ((lane >> b) & 1) ? B : ~B;
+          }
+          const int before = __popc(same & lt);
+          const int remc = __shfl_sync(0xffffffffu, rem_r, choice & 31);
+          const bool ok = !real || before < remc;
+          const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+          const uint32_t commit = bad ? (pending & ((1u << (__ffs(bad) - 1)) - 1u)) : pending;
+          if ((commit >> lane) & 1u) {
+            opt_s[jj] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
+            any_overflow |= choice == 0xFF;
+          }
+          rem_r -= __popc(mv & commit);  // lane v: committed lanes that chose v
+          avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
+          pending &= ~commit;
+          if (ARGUS_TAIL_TIMING && lane == 0) tail_ts[22]++;
         }
-        __syncwarp();
-        avail = __ballot_sync(0xffffffffu, lane < L && rem_s[lane] > 0);
-        t += take;
       }
     }
     __syncthreads();
+    TS(15);
     for (int t = tid; t < n; t += TT) {
       const int i = order_s[c0 + t];
+      const int row = byidx ? i : t;
       const int o = opt_s[t] & 0x7F;
-      uint8_t st = __ldcg(a.status + i);
-      if (opt_s[t] & 0x80) st |= 1u;         // ARGUS_ST_OVERFLOW (option 0)
-      if (!((cm_s[t] >> o) & 1u)) st |= 2u;  // ARGUS_ST_NONCOMPLIANT
+      uint8_t st = st_s[row];
+      if (opt_s[t] & 0x80) st |= 1u;              // ARGUS_ST_OVERFLOW (option 0)
+      if (!((cm_s[row] >> o) & 1u)) st |= 2u;     // ARGUS_ST_NONCOMPLIANT
       a.status[i] = st;
       a.option_out[i] = o;
     }
     __syncthreads();
   }
   if (warp == 0 && __any_sync(0xffffffffu, any_overflow) && lane == 0) atomicOr(a.flags, FLAG_OVERFLOW);
+  TS(16);
 }
 
 // ------------------------------------------------------------------ F1: PASM sampling
@@ -294,7 +388,68 @@ __device__ void select_workers(const TailArgs& a) {
 }
 
 // ------------------------------------------------------------------ the fused tail
-__global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
+// Phase M for one prompt, by the 16 lanes of a half-warp (lane hl): its P candidate lists
+// of k keys are at kp[p * S + t] (list-major, padded stride S).  Every key goes through a
+// branch-free insertion network (KM compare-exchanges into the lane's sorted register
+// list).  Keys are unique, so the order of the inputs does not matter.
+// merge_net<K>: k = K divides 16; the half-warp reads 16 / K whole lists per step (lane =
+// list offset, key), conflict-free thanks to the padded stride, with every index a
+// compile-time shift.  Measured on one SM (tools/merge_bench.cu), 148 lists of 4 keys:
+// 2.6k cycles, against 12k for the same network with a runtime k, and 7-8k for an
+// early-exit insert behind a data-dependent branch.
+template <int KM>
+__device__ __forceinline__ void net_insert(uint64_t (&v)[KM], uint64_t y) {
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {  // v stays sorted descending; y carries the smaller
+    const uint64_t hi = v[i] > y ? v[i] : y, lo = v[i] > y ? y : v[i];
+    v[i] = hi;
+    y = lo;
+  }
+}
+
+template <int KM>
+__device__ __forceinline__ void extract_topk(uint64_t (&v)[KM], int k, int hl, uint64_t* out) {
+  for (int t = 0; t < k; ++t) {  // half-warp extraction (keys unique apart from 0)
+    const uint64_t m = half_max_u64(v[0]);
+    if (hl == 0) out[t] = m;
+    if (m != 0 && v[0] == m) {
+#pragma unroll
+      for (int q = 0; q < KM - 1; ++q) v[q] = v[q + 1];
+      v[KM - 1] = 0;
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void merge_net(const uint64_t* kp, int P, int hl, bool valid, uint64_t* out) {
+  constexpr int S = 17 * K + (K & 1), G = 16 / K;
+  const int po = hl / K, to = hl % K;
+  uint64_t v[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = 0;
+  if (valid) {
+    const uint64_t* q = kp + po * S + to;
+#pragma unroll 4
+    for (int p0 = 0; p0 < P; p0 += G) net_insert<K>(v, p0 + po < P ? q[p0 * S] : 0ull);
+  }
+  extract_topk<K>(v, K, hl, out);
+}
+
+// any k <= 8: every lane takes whole lists (k = 3, 5, 6, 7)
+__device__ __forceinline__ void merge_any(const uint64_t* kp, int P, int k, int hl, bool valid, uint64_t* out) {
+  const int S = list_stride(k);
+  uint64_t v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = 0;
+  if (valid) {
+#pragma unroll 1
+    for (int p = hl; p < P; p += 16)
+      for (int t = 0; t < k; ++t) net_insert<8>(v, kp[(size_t)p * S + t]);
+  }
+  extract_topk<8>(v, k, hl, out);
+}
+
+__global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   extern __shared__ __align__(16) uint8_t smraw[];
   __shared__ int is_last;
   __shared__ uint64_t mk[PB][8];  // merged top-k keys of the block (k <= 8)
@@ -307,66 +462,89 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   const int i0 = pb * PB;
   const int nP = min(PB, a.N - i0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t T[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  uint64_t U[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (ARGUS_TAIL_TIMING) T[0] = gtimer();
+  TS(0);
+  if (ARGUS_TAIL_TIMING && tid == 0) tail_ts[20] = clock64();
+  // phase-2 option constants of lane v (init-time data, nothing upstream writes them), read
+  // before the predecessor finishes so phase 2 of the last CTA has no global round trip
+  const bool act = lane < L;
+  const float b2_v = act ? __ldg(a.b2 + lane) : 0.f;
+  const int ks_v = act ? __ldg(a.kskip + lane) : 0;
+  const float gate_v = act ? __ldg(a.gate + lane) : 0.f;
+  const float pth_v = act ? __ldg(a.pth + lane) : 0.f;
+  // layer-1 weights of this CTA's first hidden chunk (init-time data), also before the
+  // predecessor finishes: B fragments of W1x, W1s and b1 columns
+  constexpr int KSW = 8;  // k-steps per warp for d <= 1024: all B fragments in one round trip
+  const int KS = d / 16;
+  const int ks0 = KS * warp / TW, ks1 = KS * (warp + 1) / TW;
+  const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
+  uint2 bf[KSW][4];
+  float w1s_r[2][8], b1_r[2];
+  auto load_w1 = [&](int cc) {
+#pragma unroll
+    for (int q = 0; q < KSW; ++q)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        bf[q][nt] = (ks0 + q < ks1) ? __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks0 + q) * 32 + lane) : make_uint2(0, 0);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = cc * 32 + ((tid + u * TT) & 31);
+      b1_r[u] = __ldg(a.b1 + j);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
+    }
+  };
+  load_w1(blockIdx.y);
   pdl_wait();
-  if (ARGUS_TAIL_TIMING) T[1] = gtimer();
+  TS(1);
+  // inverse norms of this warp's phase-2 prompts (0 marks an invalid prompt)
+  float iq_r[PB / TW];
+#pragma unroll
+  for (int r = 0; r < PB / TW; ++r) {
+    const int p = warp + r * TW;
+    iq_r[r] = p < nP ? __ldcg(a.inv_q + i0 + p) : 1.f;
+  }
 
-  // stage the prompt block (rows past N in Xb are zero padding) with async copies
+  // ---- stage the prompt block (16 rows of Xb; rows past N are zero padding) and the
+  // block's candidate keys: list p's keys of prompts i0 .. i0 + nP - 1 are one contiguous
+  // run at (p N + i0) k, copied by one warp (16-byte cp.async when the runs are 16-byte
+  // aligned, i.e. k even, else 8-byte).  Measured: 2.4k cycles for 148 runs of 512 B,
+  // against 9k for one TMA bulk copy per run (tools/merge_bench.cu).
   for (int idx = tid; idx < PB * (d / 8); idx += TT) {
     const int p = idx / (d / 8), c = idx - p * (d / 8);
     cp_async16(xs + p * RS + c * 8, reinterpret_cast<const uint4*>(a.Xb + (int64_t)(i0 + p) * d) + c);
   }
-  if (ARGUS_TAIL_TIMING) U[0] = gtimer();
-  // ---- phase M: merge the P lists of k keys of each prompt of the block.  All of the
-  // block's keys (P slabs of 16 prompts x k, contiguous per list) arrive with one burst of
-  // async copies; then one half-warp per prompt folds them from shared memory.
-  uint64_t* kst = reinterpret_cast<uint64_t*>(ss + PB * 8);  // [P][PB][k]
-  // A list starts at (p * N + i0) * k keys: 16-byte aligned for every p only when N * k
-  // is even (and the buffer itself is); otherwise the keys move 8 bytes at a time.
-  if ((((a.N * k) & 1) | (int)(reinterpret_cast<uintptr_t>(a.keys_in) & 15)) == 0) {
-    const int slab = PB * k / 2;  // 16-byte chunks per list
-    for (int x = tid; x < a.P * slab; x += TT) {
-      const int p = x / slab, c = x - p * slab;
-      if (i0 * k + 2 * c < a.N * k)  // prompts past N: left unfilled, never read
-        cp_async16(kst + (size_t)p * PB * k + 2 * c,
-                   reinterpret_cast<const uint4*>(a.keys_in + ((int64_t)p * a.N + i0) * k) + c);
+  uint64_t* kst = reinterpret_cast<uint64_t*>(ss + PB * 8);  // [P][S(k)]
+  const int S = list_stride(k);
+  if (((k & 1) | (int)(reinterpret_cast<uintptr_t>(a.keys_in) & 15)) == 0) {
+    const int nc = nP * k / 2;  // 16-byte chunks of a run
+    for (int p = warp; p < a.P; p += TW) {
+      const uint64_t* src = a.keys_in + ((int64_t)p * a.N + i0) * k;
+      for (int c = lane; c < nc; c += 32) cp_async16(kst + (size_t)p * S + 2 * c, src + 2 * c);
     }
   } else {
-    const int slab = PB * k;  // keys per list
-    for (int x = tid; x < a.P * slab; x += TT) {
-      const int p = x / slab, e = x - p * slab;
-      if (i0 * k + e < a.N * k)  // exactly the keys of prompts < N: nothing past the buffer
-        cp_async8(kst + (size_t)p * PB * k + e, a.keys_in + ((int64_t)p * a.N + i0) * k + e);
+    const int nk = nP * k;
+    for (int p = warp; p < a.P; p += TW) {
+      const uint64_t* src = a.keys_in + ((int64_t)p * a.N + i0) * k;
+      for (int e = lane; e < nk; e += 32) cp_async8(kst + (size_t)p * S + e, src + e);
     }
   }
   cp_async_wait_all();
   __syncthreads();
-  if (ARGUS_TAIL_TIMING) U[0] = gtimer();
+  TS(2);
   {
     const int hl = lane & 15, pl = 2 * warp + (lane >> 4);
     const int i = i0 + pl;
-    TopList<8> tl;
-    tl.clear();
-    if (pl < nP) {
-      const int total = a.P * k;
-#pragma unroll 1
-      for (int e = hl; e < total; e += 16) {
-        const int p = e / k, t = e - p * k;
-        tl.insert(kst[((size_t)p * PB + pl) * k + t]);
-      }
+    const uint64_t* kp = kst + (size_t)pl * k;
+    const bool valid = pl < nP;
+    switch (k) {  // k = 0: SM mode, no candidate lists
+      case 0: break;
+      case 1: merge_net<1>(kp, a.P, hl, valid, mk[pl]); break;
+      case 2: merge_net<2>(kp, a.P, hl, valid, mk[pl]); break;
+      case 4: merge_net<4>(kp, a.P, hl, valid, mk[pl]); break;
+      case 8: merge_net<8>(kp, a.P, hl, valid, mk[pl]); break;
+      default: merge_any(kp, a.P, k, hl, valid, mk[pl]); break;
     }
-    if (ARGUS_TAIL_TIMING) U[1] = gtimer();
-    for (int t = 0; t < k; ++t) {  // half-warp extraction (keys unique apart from 0)
-      const uint64_t m = half_max_u64(tl.v[0]);
-      if (hl == 0) mk[pl][t] = m;
-      if (m != 0 && tl.v[0] == m) {
-#pragma unroll
-        for (int q = 0; q < 7; ++q) tl.v[q] = tl.v[q + 1];
-        tl.v[7] = 0;
-      }
-    }
+    TS(3);
     __syncwarp();
     if (pl < nP && hl < k) {
       const uint64_t key = mk[pl][hl];
@@ -385,9 +563,17 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
       ss[pl * k + hl] = 0.f;
     }
   }
-  if (ARGUS_TAIL_TIMING) U[2] = gtimer();
+  TS(4);
   __syncthreads();
-  if (ARGUS_TAIL_TIMING) T[2] = gtimer();
+  // the key staging area is free: prefetch W2 (rows padded to H + 4 so lane v's float4
+  // reads fall in different banks) for phase 2, in case this CTA is the block's last
+  float* w2s = reinterpret_cast<float*>(smraw + w2_offset(d, H));  // [L][H + 4]
+  const int H4 = H + 4;
+  for (int e = tid; e < L * H / 4; e += TT) {
+    const int v = e / (H / 4), j4 = e - v * (H / 4);
+    cp_async16(w2s + v * H4 + 4 * j4, a.W2 + 4 * e);
+  }
+  TS(5);
 
   // ---- phase 1: hidden units [32 cc, 32 cc + 32) for cc = blockIdx.y, blockIdx.y +
   // gridDim.y, ...; warp w takes a 1/8 slice of d.  gridDim.y = H / 32 spreads a block
@@ -395,32 +581,15 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   // candidate lists are merged once, not H / 32 times, and a pipelined tail occupies
   // few SMs while the next batch's scan starts.
   for (int cc = blockIdx.y; cc < H / 32; cc += gridDim.y) {
-    float w1s_r[2][8], b1_r[2];  // per-thread epilogue constants of this chunk
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = cc * 32 + ((tid + u * TT) & 31);
-      b1_r[u] = __ldg(a.b1 + j);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) w1s_r[u][q] = q < k ? __ldg(a.W1sT + q * H + j) : 0.f;
-    }
+    if (cc != (int)blockIdx.y) load_w1(cc);
     const int g = lane >> 2, t = lane & 3;
     const uint32_t* x32 = reinterpret_cast<const uint32_t*>(xs);
     const int RSW = RS / 2;
-    const int KS = d / 16;
-    const int ks0 = KS * warp / TW, ks1 = KS * (warp + 1) / TW;
-    const uint2* wf = reinterpret_cast<const uint2*>(a.W1xF);
     float acc[4][4];
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
-    constexpr int KSW = 8;  // k-steps per warp for d <= 1024: all B fragments in one round trip
-    uint2 bf[KSW][4];
-#pragma unroll
-    for (int q = 0; q < KSW; ++q)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-        bf[q][nt] = (ks0 + q < ks1) ? __ldg(wf + ((int64_t)(cc * 4 + nt) * KS + ks0 + q) * 32 + lane) : make_uint2(0, 0);
 #pragma unroll
     for (int q = 0; q < KSW; ++q) {
       if (ks0 + q < ks1) {
@@ -454,13 +623,16 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
     }
     __syncthreads();  // red is reused by the next chunk
   }
-  if (ARGUS_TAIL_TIMING) T[3] = gtimer();
+  TS(6);
   __threadfence();
   __syncthreads();
   if (tid == 0) is_last = atomicAdd(&a.block_cnt[pb], 1) == (int)gridDim.y - 1;
   __syncthreads();
   pdl_launch();
-  if (!is_last) return;
+  if (!is_last) {
+    cp_async_wait_all();  // the W2 prefetch lands before the CTA retires
+    return;
+  }
 
   // ---- phase 2: layer 2 + A5 for the 16 prompts of this block
   __threadfence();
@@ -473,122 +645,146 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   }
   __syncthreads();  // ss (inside the staging area) is overwritten below
   float* hs = reinterpret_cast<float*>(smraw);  // [PB][H]
-  float* w2s = hs + PB * H;                     // [L][H]
   for (int e = tid; e < PB * H / 4; e += TT) cp_async16(hs + 4 * e, a.hbuf + (int64_t)i0 * H + 4 * e);
-  const int H4 = H + 4;  // padded W2 rows: lane v's float4 reads fall in different banks
-  for (int e = tid; e < L * H / 4; e += TT) {
-    const int v = e / (H / 4), j4 = e - v * (H / 4);
-    cp_async16(w2s + v * H4 + 4 * j4, a.W2 + 4 * e);
-  }
   cp_async_wait_all();
   __syncthreads();
-  if (ARGUS_TAIL_TIMING) U[3] = gtimer();
+  TS(7);
+  // layer 2 for both of this warp's prompts at once: lane v owns option v, z_v = b2_v +
+  // sum_j W2[v][j] h_j as four interleaved partial sums per prompt.  With L <= 16 lanes v
+  // and v + 16 each take half of the hidden units of option v and add their halves with
+  // one shuffle (fadd is commutative: both lanes get the same bits).
+  const bool split = L <= 16;
+  const int ov = split ? (lane & 15) : lane;
+  float zr[PB / TW];
+  {
+    float z[PB / TW][4];
 #pragma unroll
-  for (int r = 0; r < PB / TW; ++r) {
+    for (int r = 0; r < PB / TW; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) z[r][c] = 0.f;
+    if (ov < L) {
+      const float* w2r = w2s + ov * H4;
+      const int jb = split ? (lane >> 4) * (H / 2) : 0, je = split ? jb + H / 2 : H;
+#pragma unroll 2
+      for (int j = jb; j < je; j += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(w2r + j);
+#pragma unroll
+        for (int r = 0; r < PB / TW; ++r) {
+          const float4 h4 = *reinterpret_cast<const float4*>(hs + (warp + r * TW) * H + j);
+          z[r][0] = __fmaf_rn(w4.x, h4.x, z[r][0]);
+          z[r][1] = __fmaf_rn(w4.y, h4.y, z[r][1]);
+          z[r][2] = __fmaf_rn(w4.z, h4.z, z[r][2]);
+          z[r][3] = __fmaf_rn(w4.w, h4.w, z[r][3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < PB / TW; ++r) {
+      float zz = (ov < L) ? __fadd_rn(__fadd_rn(z[r][0], z[r][1]), __fadd_rn(z[r][2], z[r][3])) : 0.f;
+      if (split) zz = __fadd_rn(zz, __shfl_xor_sync(0xffffffffu, zz, 16));
+      zr[r] = zz;
+    }
+  }
+  TS(8);
+  // A5 for both prompts of the warp together (independent chains interleave): r_v, masks,
+  // the preference rank of v and the optimal option, from per-warp shared tables of r and
+  // p_th (broadcast reads in unrolled loops; no shuffle chains, no data-dependent branches)
+  constexpr int R = PB / TW;
+  float* rr_s = reinterpret_cast<float*>(smraw + w2_offset(d, H) + sizeof(float) * (size_t)L * H4) + warp * R * 32;
+  float* pth_s = reinterpret_cast<float*>(smraw + w2_offset(d, H) + sizeof(float) * (size_t)L * H4) + TW * R * 32;
+  if (warp == 0) pth_s[lane] = pth_v;
+  float rr[R];
+  uint32_t amask[R], cmask[R];
+  bool adm[R], cmp[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    rr[r] = 0.f;
+    if (act) {
+      const float z = __fadd_rn(zr[r], b2_v);
+      rr[r] = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
+      if (lane == 0) rr[r] = 1.0f;
+    }
+    rr_s[r * 32 + lane] = rr[r];
+    const float s1 = s1_r[r];
+    adm[r] = act && (lane == 0 || ks_v == 0 || s1 >= gate_v);
+    cmp[r] = adm[r] && rr[r] >= a.delta;
+    amask[r] = __ballot_sync(0xffffffffu, adm[r]);
+    cmask[r] = __ballot_sync(0xffffffffu, cmp[r]);
+  }
+  const uint32_t gmask = __ballot_sync(0xffffffffu, act && ks_v != 0);
+  uint32_t pmask[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) pmask[r] = __ballot_sync(0xffffffffu, act && ks_v != 0 && s1_r[r] >= gate_v);
+  __syncthreads();  // rr_s of every warp, pth_s
+  TS(21);
+  int rank[R], oi[R];
+  float bp[R], br[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    rank[r] = 0;
+    oi[r] = 0;
+    bp[r] = -INFINITY;
+    br[r] = -INFINITY;
+  }
+  // rank of v in pi_i: admissible options before it by (r desc, p_th desc, index asc); o_i
+  // (DESIGN R18): the compliant option with the largest p_th, then the larger
+  // r, then the lower index -- a running best over u ascending (ties keep the lower u)
+#pragma unroll 4
+  for (int u = 0; u < L; ++u) {
+    const float pu = pth_s[u];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float ru = rr_s[r * 32 + u];
+      const bool before = ((amask[r] >> u) & 1u) &&
+                          (ru > rr[r] || (ru == rr[r] && (pu > pth_v || (pu == pth_v && u < lane))));
+      rank[r] += before ? 1 : 0;
+      const bool better = ((cmask[r] >> u) & 1u) && (pu > bp[r] || (pu == bp[r] && ru > br[r]));
+      bp[r] = better ? pu : bp[r];
+      br[r] = better ? ru : br[r];
+      oi[r] = better ? u : oi[r];
+    }
+  }
+  TS(18);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
     const int p = warp + r * TW;
     if (p >= nP) break;
     const int i = i0 + p;
-    const bool act = lane < L;
-    // lane v owns option v: z_v = b2_v + sum_j W2[v][j] h_j, four interleaved partial
-    // sums in a compact (not unrolled) loop -- this phase runs once per CTA from a cold
-    // instruction cache, so code size, not arithmetic, is what costs here
-    // With L <= 16 lanes v and v + 16 each take half of the hidden units of option v
-    // and add their halves with one shuffle (fadd is commutative: both lanes get the
-    // same bits), halving the loop on the tail's critical path.
-    float z = 0.f;
-    const bool split = L <= 16;
-    const int ov = split ? (lane & 15) : lane;
-    if (ov < L) {
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      const float* w2r = w2s + ov * H4;
-      const float* hp = hs + p * H;
-      const int jb = split ? (lane >> 4) * (H / 2) : 0, je = split ? jb + H / 2 : H;
-#pragma unroll 1
-      for (int j = jb; j < je; j += 4) {
-        const float4 w4 = *reinterpret_cast<const float4*>(w2r + j);
-        const float4 h4 = *reinterpret_cast<const float4*>(hp + j);
-        z0 = __fmaf_rn(w4.x, h4.x, z0);
-        z1 = __fmaf_rn(w4.y, h4.y, z1);
-        z2 = __fmaf_rn(w4.z, h4.z, z2);
-        z3 = __fmaf_rn(w4.w, h4.w, z3);
-      }
-      z = __fadd_rn(__fadd_rn(z0, z1), __fadd_rn(z2, z3));
-    }
-    if (split) z = __fadd_rn(z, __shfl_xor_sync(0xffffffffu, z, 16));
-    float rr = 0.f;
-    if (act) {
-      z = __fadd_rn(z, a.b2[lane]);
-      rr = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
-      if (lane == 0) rr = 1.0f;
-    }
-    const float s1 = s1_r[r];
-    const int ks_ = act ? a.kskip[lane] : 0;
-    const float gate = act ? a.gate[lane] : 0.f;
-    const bool gated_pass = act && ks_ != 0 && s1 >= gate;
-    const bool adm = act && (lane == 0 || ks_ == 0 || s1 >= gate);
-    const bool cmp = adm && rr >= a.delta;
-    const uint32_t amask = __ballot_sync(0xffffffffu, adm);
-    const uint32_t cmask = __ballot_sync(0xffffffffu, cmp);
-    const uint32_t gmask = __ballot_sync(0xffffffffu, act && ks_ != 0);
-    const uint32_t pmask = __ballot_sync(0xffffffffu, gated_pass);
-    const float pth = act ? a.pth[lane] : 0.f;
-    int rank = 0;
-    for (int u = 0; u < L; ++u) {
-      const float ru = __shfl_sync(0xffffffffu, rr, u);
-      const float pu = __shfl_sync(0xffffffffu, pth, u);
-      const bool before = ((amask >> u) & 1u) &&
-                          (ru > rr || (ru == rr && (pu > pth || (pu == pth && u < lane))));
-      rank += before ? 1 : 0;
-    }
-    if (act) a.rhat[(int64_t)i * L + lane] = rr;
+    if (act) a.rhat[(int64_t)i * L + lane] = rr[r];
     // pi_i as a list: admissible option v at its position, 0xFF after the last
-    if (adm) a.prefl[(int64_t)i * a.Lw + rank] = (uint8_t)lane;
-    if (lane < a.Lw && lane >= __popc(amask)) a.prefl[(int64_t)i * a.Lw + lane] = 0xFF;
-    // optimal option o_i: the compliant option with the largest p_th, then
-    // the larger r, then the lower index (DESIGN R18); option 0 is always compliant
-    float kp = cmp ? pth : -INFINITY, kr = cmp ? rr : -INFINITY;
-    int kv = lane;
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      const float op = __shfl_xor_sync(0xffffffffu, kp, s), orr = __shfl_xor_sync(0xffffffffu, kr, s);
-      const int ov = __shfl_xor_sync(0xffffffffu, kv, s);
-      if (op > kp || (op == kp && (orr > kr || (orr == kr && ov < kv)))) {
-        kp = op;
-        kr = orr;
-        kv = ov;
-      }
-    }
-    const int oi = kp == -INFINITY ? 0 : kv;
-    uint8_t st = (gmask != 0 && pmask == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
+    if (adm[r]) a.prefl[(int64_t)i * a.Lw + rank[r]] = (uint8_t)lane;
+    if (lane < a.Lw && lane >= __popc(amask[r])) a.prefl[(int64_t)i * a.Lw + lane] = 0xFF;
+    uint8_t st = (gmask != 0 && pmask[r] == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
     if (a.policy == 1) {
       // PASM sample: u = Philox word >> 8 scaled by 2^-24 (exact), the
       // first option whose float32 running sum exceeds u, then the gate fallback
       const uint32_t x0 = philox_x0((uint32_t)i, a.seq_lo, a.seq_hi, 0u, a.seed_lo, a.seed_hi);
       const float u = (float)(x0 >> 8) * 5.9604644775390625e-8f;
-      const bool hit = act && u < a.pasm_cdf[oi * 32 + lane];
+      const bool hit = act && u < a.pasm_cdf[oi[r] * 32 + lane];
       const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-      const int as = hm ? __ffs(hm) - 1 : (int)a.pasm_last[oi];
-      const uint32_t below = amask & (as >= 31 ? 0xffffffffu : ((2u << as) - 1u));
+      const int as = hm ? __ffs(hm) - 1 : (int)a.pasm_last[oi[r]];
+      const uint32_t below = amask[r] & (as >= 31 ? 0xffffffffu : ((2u << as) - 1u));
       const int af = 31 - __clz(below);  // bit 0 is always admissible
       if (lane == 0) {
         a.option_out[i] = af;
-        if (!((cmask >> af) & 1u)) st |= 2u;  // ARGUS_ST_NONCOMPLIANT
+        if (!((cmask[r] >> af) & 1u)) st |= 2u;  // ARGUS_ST_NONCOMPLIANT
       }
     }
     if (lane == 0) {
       // K6 flags a non-finite / zero-norm prompt only where it runs (the root); every
       // rank sees the broadcast inv_q = 0 of that prompt, so every rank fails the call
-      if (__ldg(a.inv_q + i) == 0.f) atomicOr(a.flags, FLAG_INVALID_INPUT);
-      a.ccount[i] = (uint8_t)__popc(cmask);
-      a.cmask[i] = cmask;
+      if (iq_r[r] == 0.f) atomicOr(a.flags, FLAG_INVALID_INPUT);
+      a.ccount[i] = (uint8_t)__popc(cmask[r]);
+      a.cmask[i] = cmask[r];
       a.status[i] = st;
-      if (a.optimal_out) a.optimal_out[i] = oi;
-      if (a.aff_win > 0 && i >= a.N - a.aff_win) a.aff_ring[(a.aff_pos0 + i) % a.aff_win] = (uint8_t)oi;
+      if (a.optimal_out) a.optimal_out[i] = oi[r];
+      if (a.aff_win > 0 && i >= a.N - a.aff_win) a.aff_ring[(a.aff_pos0 + i) % a.aff_win] = (uint8_t)oi[r];
     }
   }
+  TS(19);
 
   // ---- phase 3: the last block to finish phase 2 runs the assignment for all N
-  if (ARGUS_TAIL_TIMING) T[4] = gtimer();
+  TS(9);
   __threadfence();
   __syncthreads();
   if (tid == 0) is_last = atomicAdd(a.launch_cnt, 1) == (int)gridDim.x - 1;
@@ -596,20 +792,24 @@ __global__ void __launch_bounds__(TT) k_tail(TailArgs a) {
   if (!is_last) return;
   __threadfence();
   if (tid == 0) *a.launch_cnt = 0;
-  if (ARGUS_TAIL_TIMING) T[5] = gtimer();
+  TS(10);
   if (a.policy == 0) assign_all(a, smraw);
   if (a.n_workers > 0) {
     __syncthreads();  // option_out of this CTA's own phase 3 is visible to the block
     select_workers(a);
   }
   if (ARGUS_TAIL_TIMING) {
-    T[6] = gtimer();
-    if (tid == 0)
-      printf("[tail] N=%d pdl %llu | pre-merge %llu loads %llu extract %llu cpwait %llu | layer1 %llu | ticket+stage2 %llu l2+A5 %llu | ticket %llu | assign %llu ns\n",
-             a.N, (unsigned long long)(T[1] - T[0]), (unsigned long long)(U[0] - T[1]),
-             (unsigned long long)(U[1] - U[0]), (unsigned long long)(U[2] - U[1]), (unsigned long long)(T[2] - U[2]),
-             (unsigned long long)(T[3] - T[2]), (unsigned long long)(U[3] - T[3]), (unsigned long long)(T[4] - U[3]),
-             (unsigned long long)(T[5] - T[4]), (unsigned long long)(T[6] - T[5]));
+    __syncthreads();
+    TS(11);
+    if (tid == 0) {
+      const unsigned long long c1 = clock64();
+      const unsigned long long* t = tail_ts;
+      printf("[tail] N=%d MHz %.0f | pdl %llu stage %llu merge %llu out %llu w2 %llu layer1 %llu | ticket+h %llu l2dot %llu A5 %llu "
+             "| ticket %llu | assign: load %llu sort %llu sd %llu write %llu | total %llu ns | P %d | A5[0]: sigm %llu rank %llu omax %llu | sd steps %llu\n",
+             a.N, 1e3 * (double)(c1 - t[20]) / (double)(t[11] - t[0]), t[1] - t[0], t[2] - t[1], t[3] - t[2],
+             t[4] - t[3], t[5] - t[4], t[6] - t[5], t[7] - t[6], t[8] - t[7], t[9] - t[8], t[10] - t[9],
+             t[13] - t[12], t[14] - t[13], t[15] - t[14], t[16] - t[15], t[11] - t[0], a.P, t[21] - t[8], t[18] - t[21], t[19] - t[18], t[22]);
+    }
   }
 }
 

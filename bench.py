@@ -283,7 +283,7 @@ def main():
     stream = torch.cuda.Stream()
     r = argus.Router(d, k, opts, W1, b1, W2, b2, capacity=cfg.M, max_batch=max_batch, rank=rank, world=world,
                      device=local_rank, nccl_unique_id=uid, stream=stream.cuda_stream,
-                     pipeline=bool(args.pipeline) and world == 1 and uid is None)
+                     pipeline=bool(args.pipeline))
 
     # ---- cache: generated chunk by chunk on rank 0 only, inserted through the ABI (the
     # library broadcasts rank 0's rows; every rank keeps its stripe, so no rank holds more
@@ -507,9 +507,11 @@ def main():
             "parallelism": f"cache row-striped over {world} GPU(s)",
             "l2": f"inputs larger than L2 (cache shard {bytes_per_launch / 1e9:.2f} GB >> 126 MB L2)",
             "insert_s": round(t_insert, 2),
-            "pipeline": ("tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline=1); every "
-                         "batch's outputs are complete inside the timed region")
-                        if (args.pipeline and world == 1) else "off",
+            "pipeline": (("tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline=1); every "
+                          "batch's outputs are complete inside the timed region")
+                         + ("; NCCL: bcast(b+1) is issued before the all-gather of b on one comm stream"
+                            if (world > 1 or args.force_nccl) else ""))
+                        if args.pipeline else "off",
             "ranks_hold": "rank 0 generates the cache and prompts; the library broadcasts them, every rank keeps "
                           "its stripe" if world > 1 else "one GPU holds the whole cache",
         },

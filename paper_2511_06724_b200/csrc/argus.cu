@@ -121,8 +121,8 @@ struct argus_router {
   int32_t* d_ctr[2] = {nullptr, nullptr};    // [CTR_WORDS] scan work / visit counters
   uint64_t* d_partial[2] = {nullptr, nullptr};  // [P * N <= partial_lists][k] per batch parity
   int64_t partial_lists = 0;
-  uint64_t* d_keys = nullptr;      // [max_batch][k]
-  uint64_t* d_keys_all = nullptr;  // [world][max_batch][k]
+  uint64_t* d_keys[2] = {nullptr, nullptr};      // [max_batch][k] this shard's merged keys, per parity
+  uint64_t* d_keys_all[2] = {nullptr, nullptr};  // [world][max_batch][k] all-gathered keys, per parity
   float* d_score = nullptr;        // [max_batch][k]
   uint32_t* d_idx = nullptr;       // [max_batch][k]
   float* d_rhat = nullptr;         // [max_batch][L]
@@ -173,7 +173,29 @@ struct argus_router {
   int32_t n_workers = 0;
   int16_t* d_wlist = nullptr;      // [32][32]
   int32_t* d_wcount = nullptr;     // [32]
-  int32_t* d_quota = nullptr;      // [32] quotas broadcast from rank 0 (NCCL mode, route_batch*)
+  int32_t* d_quota[2] = {nullptr, nullptr};  // [32] quotas broadcast from rank 0 (NCCL mode), per parity
+  // pipelined NCCL mode: every collective on one stream in program order (identical on all
+  // ranks), and the all-gather + tail of batch b deferred until call b+1 has issued its
+  // broadcast, so the comm stream runs bcast(b+1) before AG(b) and the scans run back to back
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bcast[2] = {nullptr, nullptr};  // batch with parity q broadcast
+  cudaEvent_t ev_ag[2] = {nullptr, nullptr};     // its candidate keys all-gathered
+  struct Deferred {
+    bool valid = false;
+    int q = 0, N = 0, P = 0;
+    bool qdev = false;
+    int32_t quota[32];
+    int32_t* option = nullptr;
+    uint32_t* idx = nullptr;
+    float* score = nullptr;
+    float* quality = nullptr;
+    uint8_t* status = nullptr;
+    argus_route_extra ex{nullptr, nullptr, nullptr};
+    bool has_ex = false;
+    uint32_t* flags = nullptr;
+    int async_slot = -1;  // argus_route_batch_async slot whose result copy follows the tail
+    size_t async_bytes = 0;
+  } def;
   float* d_wtime = nullptr;        // [MAX_WORKERS]
   int32_t* d_queue = nullptr;      // [MAX_WORKERS]
   uint64_t* d_handle = nullptr;    // [capacity] latent handles by cache position (replicated on every rank)
@@ -427,11 +449,12 @@ int argus_route_destroy(argus_router* r) {
   if (!r) return ARGUS_E_INVALID;
   cudaSetDevice(r->cfg.device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream})
+  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream, r->comm_stream})
     if (s) cudaStreamSynchronize(s);
   void* ptrs[] = {r->d_kskip, r->d_pth, r->d_gate, r->d_W1xF, r->d_W1sT, r->d_b1, r->d_W2, r->d_b2, r->d_h,
                   r->d_mlp_cnt, r->d_tail_cnt, r->d_Cb, r->d_invc, r->d_Xstage, r->d_Xb[0], r->d_Xb[1],
-                  r->d_invq[0], r->d_invq[1], r->d_partial[0], r->d_partial[1], r->d_keys, r->d_keys_all,
+                  r->d_invq[0], r->d_invq[1], r->d_partial[0], r->d_partial[1], r->d_keys[0], r->d_keys[1],
+                  r->d_keys_all[0], r->d_keys_all[1], r->d_quota[0], r->d_quota[1],
                   r->d_score, r->d_idx, r->d_rhat, r->d_pref, r->d_ccount, r->d_cmask, r->d_status, r->d_option,
                   r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1], r->d_cdf, r->d_plast,
                   r->d_aff, r->d_wlist, r->d_wcount, r->d_wtime, r->d_queue, r->d_optimal, r->d_worker,
@@ -455,9 +478,9 @@ int argus_route_destroy(argus_router* r) {
   for (auto e : r->ev_pool) cudaEventDestroy(e);
   if (r->comm) nccl().CommDestroy(r->comm);
   for (int q = 0; q < 2; ++q)
-    for (cudaEvent_t e : {r->ev_in[q], r->ev_prep[q], r->ev_scan[q], r->ev_tail[q]})
+    for (cudaEvent_t e : {r->ev_in[q], r->ev_prep[q], r->ev_scan[q], r->ev_tail[q], r->ev_bcast[q], r->ev_ag[q]})
       if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream})
+  for (cudaStream_t s : {r->prep_stream, r->scan_stream, r->tail_stream, r->comm_stream})
     if (s) cudaStreamDestroy(s);
   if (r->own_stream && r->stream) cudaStreamDestroy(r->stream);
   delete r;
@@ -516,7 +539,9 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) { delete r; return ARGUS_E_CUDA; }
     r->own_stream = true;
   }
-  r->pipe = c.pipeline != 0 && c.world == 1 && c.nccl_unique_id == nullptr;
+  // pipelining: one GPU, or NCCL mode (one communicator, collectives in program order on
+  // the comm stream); not the external mode, whose caller moves the keys itself
+  r->pipe = c.pipeline != 0 && (c.world == 1 || c.nccl_unique_id != nullptr);
   r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
   if (const char* e = getenv("ARGUS_SCAN_RESERVE")) r->scan_reserve = std::min(std::max(atoi(e), 0), 16);
@@ -527,8 +552,11 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     bool ok = cudaStreamCreateWithPriority(&r->prep_stream, cudaStreamNonBlocking, hi) == cudaSuccess &&
               cudaStreamCreateWithPriority(&r->scan_stream, cudaStreamNonBlocking, lo) == cudaSuccess &&
               cudaStreamCreateWithPriority(&r->tail_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
+    if (ok && c.nccl_unique_id) ok = cudaStreamCreateWithPriority(&r->comm_stream, cudaStreamNonBlocking, hi) == cudaSuccess;
     for (int q = 0; q < 2 && ok; ++q)
-      ok = cudaEventCreateWithFlags(&r->ev_in[q], cudaEventDisableTiming) == cudaSuccess &&
+      ok = cudaEventCreateWithFlags(&r->ev_bcast[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&r->ev_ag[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&r->ev_in[q], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&r->ev_prep[q], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&r->ev_scan[q], cudaEventDisableTiming) == cudaSuccess &&
            cudaEventCreateWithFlags(&r->ev_tail[q], cudaEventDisableTiming) == cudaSuccess;
@@ -580,8 +608,11 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     TRY_RC(dalloc(r, &r->d_gthr[q], (size_t)r->n_pad_max));
     TRY_RC(dalloc(r, &r->d_ctr[q], CTR_WORDS));
   }
-  TRY_RC(dalloc(r, &r->d_keys, (size_t)c.max_batch * k));
-  TRY_RC(dalloc(r, &r->d_keys_all, (size_t)G * c.max_batch * k));
+  for (int q = 0; q < 2; ++q) {
+    TRY_RC(dalloc(r, &r->d_keys[q], (size_t)c.max_batch * k));
+    TRY_RC(dalloc(r, &r->d_keys_all[q], (size_t)G * c.max_batch * k));
+    TRY_RC(dalloc(r, &r->d_quota[q], 32));
+  }
   TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_idx, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_rhat, (size_t)c.max_batch * L));
@@ -596,7 +627,6 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_aff, ARGUS_AFFINITY_WINDOW));
   TRY_RC(dalloc(r, &r->d_wlist, 32 * 32));
   TRY_RC(dalloc(r, &r->d_wcount, 32));
-  TRY_RC(dalloc(r, &r->d_quota, 32));
   TRY_RC(dalloc(r, &r->d_wtime, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_queue, MAX_WORKERS));
   TRY_RC(dalloc(r, &r->d_optimal, (size_t)c.max_batch));
@@ -872,25 +902,32 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     StageScope sc(r, ARGUS_STAGE_PREP, s_prep);
     launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q],
                         r->flags_cur ? r->flags_cur : r->d_flags,
-                        s_prep, !pipelined, quota_bcast ? quota : nullptr, r->cfg.L, r->d_quota);
+                        s_prep, !pipelined, quota_bcast ? quota : nullptr, r->cfg.L, r->d_quota[q]);
     LAUNCHED(r);
   }
   if (!root) {
-    CU_TRY(r, cudaMemsetAsync(r->d_gthr[q], 0, sizeof(uint64_t) * (size_t)n_pad, r->stream));
-    CU_TRY(r, cudaMemsetAsync(r->d_ctr[q], 0, sizeof(int32_t) * CTR_WORDS, r->stream));
+    CU_TRY(r, cudaMemsetAsync(r->d_gthr[q], 0, sizeof(uint64_t) * (size_t)n_pad, s_prep));
+    CU_TRY(r, cudaMemsetAsync(r->d_ctr[q], 0, sizeof(int32_t) * CTR_WORDS, s_prep));
   }
+  // C-1 (NCCL mode): rank 0's bf16 batch, inverse norms (and quotas) to every rank; in
+  // pipelined mode on the comm stream, in program order with the deferred all-gathers
+  cudaStream_t s_bc = (pipelined && nccl_mode(r)) ? r->comm_stream : s_scan;
   if (pipelined) {
     CU_TRY(r, cudaEventRecord(r->ev_prep[q], s_prep));
-    CU_TRY(r, cudaStreamWaitEvent(s_scan, r->ev_prep[q], 0));
+    CU_TRY(r, cudaStreamWaitEvent(s_bc, r->ev_prep[q], 0));
     CU_TRY(r, cudaStreamWaitEvent(r->stream, r->ev_prep[q], 0));  // the prompt buffer is consumed
   }
   r->cur = q;
   if (nccl_mode(r)) {
     NC_TRY(r, nccl().GroupStart());
-    NC_TRY(r, nccl().Broadcast(r->d_Xb[q], r->d_Xb[q], (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, r->stream));
-    NC_TRY(r, nccl().Broadcast(r->d_invq[q], r->d_invq[q], (size_t)n_pad, ncclFloat32, 0, r->comm, r->stream));
-    if (quota_bcast) NC_TRY(r, nccl().Broadcast(r->d_quota, r->d_quota, 32, ncclInt32, 0, r->comm, r->stream));
+    NC_TRY(r, nccl().Broadcast(r->d_Xb[q], r->d_Xb[q], (size_t)n_pad * d * 2, ncclUint8, 0, r->comm, s_bc));
+    NC_TRY(r, nccl().Broadcast(r->d_invq[q], r->d_invq[q], (size_t)n_pad, ncclFloat32, 0, r->comm, s_bc));
+    if (quota_bcast) NC_TRY(r, nccl().Broadcast(r->d_quota[q], r->d_quota[q], 32, ncclInt32, 0, r->comm, s_bc));
     NC_TRY(r, nccl().GroupEnd());
+    if (s_bc != s_scan) {
+      CU_TRY(r, cudaEventRecord(r->ev_bcast[q], s_bc));
+      CU_TRY(r, cudaStreamWaitEvent(s_scan, r->ev_bcast[q], 0));
+    }
   }
   if (k == 0) {  // SM mode: no cache scan, the tail sees the prompts only
     *P_out = 0;
@@ -925,7 +962,8 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // still saturate HBM) leaves a few SMs free so the next batch's prep and this batch's
   // tail run beside it instead of queueing behind the persistent grid (N = 48, fixed:
   // 264 -> 256 us per batch with 2 SMs reserved, scripts/scan_reserve_sweep.sh)
-  const int scan_sms = pipelined && N <= 128 ? r->num_sms - r->scan_reserve : r->num_sms;
+  // (pipelined NCCL mode: always, so the collectives of the neighbouring batches find SMs)
+  const int scan_sms = pipelined && (N <= 128 || nccl_mode(r)) ? r->num_sms - r->scan_reserve : r->num_sms;
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
     if (pair) {
@@ -967,8 +1005,8 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   *P_out = a.P;
   if (keys_dev) {
     {
-      StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL);
-      launch_merge_topk(r->d_partial[q], a.P, N, k, keys_dev, nullptr, nullptr, r->stream);
+      StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL, s_scan);
+      launch_merge_topk(r->d_partial[q], a.P, N, k, keys_dev, nullptr, nullptr, s_scan);
     }
     LAUNCHED(r);
   }
@@ -978,7 +1016,9 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 // The fused tail (merge of P candidate lists per prompt, predictor, A5, assignment).
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr);
+                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr,
+                       int q = -1);
+static int flush_deferred(argus_router* r);
 static int async_harvest(argus_router* r, int q);
 // route_batch* in NCCL mode: the quotas are rank 0's (broadcast), other ranks may pass NULL
 static bool quota_from_root(const argus_router* r) {
@@ -1006,7 +1046,8 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
 
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex) {
+                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex, int q) {
+  if (q < 0) q = r->cur;  // the parity of the buffers this batch's partial_impl used
   const bool qdev = r->quota_dev_next;  // consumed by this call whatever happens
   r->quota_dev_next = false;
   int rc = check_state(r);
@@ -1021,8 +1062,8 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.P = P;
   m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
   m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
-  m.Xb = r->d_Xb[r->cur];  // the bf16 copy of this batch made by partial_impl
-  m.inv_q = r->d_invq[r->cur];
+  m.Xb = r->d_Xb[q];  // the bf16 copy of this batch made by partial_impl
+  m.inv_q = r->d_invq[q];
   m.W1xF = r->d_W1xF;
   m.W1sT = r->d_W1sT;
   m.b1 = r->d_b1;
@@ -1047,7 +1088,7 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)
   for (int v = 0; v < 32; ++v) m.quota[v] = (v < L && quota) ? quota[v] : 0;
-  m.quota_dev = qdev ? r->d_quota : nullptr;
+  m.quota_dev = qdev ? r->d_quota[q] : nullptr;
   m.option_out = option_out_dev ? option_out_dev : r->d_option;
   m.status = status_dev ? status_dev : r->d_status;
   m.flags = r->flags_cur ? r->flags_cur : r->d_flags;
@@ -1104,6 +1145,42 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     return ARGUS_E_INVALID;
   r->pending = true;
   int32_t P = 0;
+  if (r->pipe && !r->serial_call && nccl_mode(r)) {
+    // Pipelined NCCL mode.  This call: K6 (root) -> C-1 broadcast on the comm stream ->
+    // scan + K5 local merge on the scan stream.  Then the previous batch's C-2 all-gather
+    // (comm stream, behind this broadcast) and tail (tail stream) are issued, and this
+    // batch's wait for the next call or argus_route_join.  Every rank issues the
+    // collectives in the same order: bcast(b), AG(b-1), bcast(b+1), AG(b), ...
+    const int q = (int)(r->seq & 1);
+    CU_TRY(r, cudaEventRecord(r->ev_in[q], r->stream));
+    CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_in[q], 0));
+    if (r->tail_inflight[q]) CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_tail[q], 0));  // parity q free
+    const bool qb = quota_from_root(r);
+    rc = partial_impl(r, prompts_dev, N, r->cfg.k > 0 ? r->d_keys[q] : nullptr, &P, q, r->prep_stream,
+                      r->scan_stream, qb, quota);
+    if (rc) return rc;
+    CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->scan_stream));
+    rc = flush_deferred(r);
+    if (rc) return rc;
+    argus_router::Deferred& D = r->def;
+    D.valid = true;
+    D.q = q;
+    D.N = N;
+    D.P = P;
+    D.qdev = qb;
+    for (int v = 0; v < 32; ++v) D.quota[v] = (v < r->cfg.L && quota) ? quota[v] : 0;
+    D.option = option_out_dev;
+    D.idx = topk_idx_dev;
+    D.score = topk_score_dev;
+    D.quality = quality_dev;
+    D.status = status_dev;
+    D.has_ex = ex != nullptr;
+    if (ex) D.ex = *ex;
+    D.flags = r->flags_cur;
+    D.async_slot = -1;
+    r->seq++;
+    return ARGUS_OK;
+  }
   if (r->pipe && !r->serial_call) {  // prep / scan / tail on the internal streams (see the file header)
     const int q = (int)(r->seq & 1);
     CU_TRY(r, cudaEventRecord(r->ev_in[q], r->stream));  // prompts (and earlier inserts) are ready
@@ -1128,20 +1205,57 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
                        status_dev, r->stream, true, ex);
   }
   const bool qb = quota_from_root(r);
-  rc = partial_impl(r, prompts_dev, N, r->d_keys, &P, 0, nullptr, nullptr, qb, quota);
+  rc = partial_impl(r, prompts_dev, N, r->d_keys[0], &P, 0, nullptr, nullptr, qb, quota);
   if (rc) return rc;
   r->quota_dev_next = qb;
   // C-2: N*k candidate keys from every shard
   if (r->cfg.k > 0)
-    NC_TRY(r, nccl().AllGather(r->d_keys, r->d_keys_all, (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
-  return finish_impl(r, r->d_keys_all, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
+    NC_TRY(r, nccl().AllGather(r->d_keys[0], r->d_keys_all[0], (size_t)N * r->cfg.k, ncclUint64, r->comm, r->stream));
+  return finish_impl(r, r->d_keys_all[0], r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
                      quality_dev, status_dev, r->stream, true, ex);
+}
+
+// Pipelined NCCL mode: issue the deferred batch's C-2 all-gather (comm stream, after its
+// scan) and its tail (tail stream), then the result copy of an asynchronous host call.
+static int flush_deferred(argus_router* r) {
+  argus_router::Deferred& D = r->def;
+  if (!D.valid) return ARGUS_OK;
+  D.valid = false;
+  const int q = D.q, k = r->cfg.k;
+  if (k > 0) {
+    CU_TRY(r, cudaStreamWaitEvent(r->comm_stream, r->ev_scan[q], 0));
+    NC_TRY(r, nccl().AllGather(r->d_keys[q], r->d_keys_all[q], (size_t)D.N * k, ncclUint64, r->comm,
+                               r->comm_stream));
+    CU_TRY(r, cudaEventRecord(r->ev_ag[q], r->comm_stream));
+    CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_ag[q], 0));
+  } else {  // SM mode: the broadcast batch is the whole input (the scan stream waited for it)
+    CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_scan[q], 0));
+  }
+  uint32_t* saved = r->flags_cur;
+  r->flags_cur = D.flags;
+  r->quota_dev_next = D.qdev;
+  int rc = finish_impl(r, r->d_keys_all[q], r->cfg.world, D.N, D.quota, D.option, D.idx, D.score, D.quality,
+                       D.status, r->tail_stream, false, D.has_ex ? &D.ex : nullptr, q);
+  r->flags_cur = saved;
+  if (rc) return rc;
+  CU_TRY(r, cudaEventRecord(r->ev_tail[q], r->tail_stream));
+  r->tail_inflight[q] = true;
+  if (D.async_slot >= 0) {  // argus_route_batch_async: one packed copy of the results
+    const int a = D.async_slot;
+    CU_TRY(r, cudaEventRecord(r->ev_done[a], r->tail_stream));
+    CU_TRY(r, cudaStreamWaitEvent(r->d2h_stream, r->ev_done[a], 0));
+    CU_TRY(r, cudaMemcpyAsync(r->h_oasync[a], r->d_oasync[a], D.async_bytes, cudaMemcpyDeviceToHost, r->d2h_stream));
+    CU_TRY(r, cudaEventRecord(r->ev_async[a], r->d2h_stream));
+  }
+  return ARGUS_OK;
 }
 
 int argus_route_join(argus_router* r, void* stream) {
   if (!r) return ARGUS_E_INVALID;
   if (r->poisoned) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
+  int rc0 = flush_deferred(r);
+  if (rc0) return rc0;
   cudaStream_t s = stream ? (cudaStream_t)stream : r->stream;
   for (int q = 0; q < 2; ++q)
     if (r->tail_inflight[q]) {
@@ -1260,6 +1374,10 @@ static int flags_rc(uint32_t fl) {
 // Finish the call carried by parity slot q (if any): wait for its D2H, keep its rc.
 static int async_harvest(argus_router* r, int q) {
   if (r->async_ticket[q] < 0) return ARGUS_OK;
+  if (r->def.valid && r->def.async_slot == q) {  // its tail (and copy) not issued yet
+    int rc = flush_deferred(r);
+    if (rc) return rc;
+  }
   CU_TRY(r, cudaEventSynchronize(r->ev_async[q]));
   // one packed copy landed in pinned staging: unpack into the caller's buffers
   const argus_router::AsyncOut& o = r->aout[q];
@@ -1316,12 +1434,17 @@ int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, co
   if (rc) return rc;
   // results: one packed device-to-host copy on the copy stream once this call's tail
   // is done (the tail stream itself is never held up by copies); harvest unpacks it
-  cudaStream_t s = (r->pipe && r->tail_inflight[(r->seq - 1) & 1]) ? r->tail_stream : r->stream;
-  CU_TRY(r, cudaEventRecord(r->ev_done[q], s));
-  CU_TRY(r, cudaStreamWaitEvent(r->d2h_stream, r->ev_done[q], 0));
   const size_t o_end = o_st + (size_t)N;
-  CU_TRY(r, cudaMemcpyAsync(r->h_oasync[q], D, o_end, cudaMemcpyDeviceToHost, r->d2h_stream));
-  CU_TRY(r, cudaEventRecord(r->ev_async[q], r->d2h_stream));
+  if (r->def.valid) {  // pipelined NCCL mode: the tail is issued later, the copy with it
+    r->def.async_slot = q;
+    r->def.async_bytes = o_end;
+  } else {
+    cudaStream_t s = (r->pipe && r->tail_inflight[(r->seq - 1) & 1]) ? r->tail_stream : r->stream;
+    CU_TRY(r, cudaEventRecord(r->ev_done[q], s));
+    CU_TRY(r, cudaStreamWaitEvent(r->d2h_stream, r->ev_done[q], 0));
+    CU_TRY(r, cudaMemcpyAsync(r->h_oasync[q], D, o_end, cudaMemcpyDeviceToHost, r->d2h_stream));
+    CU_TRY(r, cudaEventRecord(r->ev_async[q], r->d2h_stream));
+  }
   r->aout[q] = {N, option_out, topk_idx, topk_score, quality_out, status_out};
   r->async_ticket[q] = r->next_ticket;
   *ticket = r->next_ticket++;

@@ -223,6 +223,25 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
                            uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                            uint8_t* status_dev);
 
+/* Fused candidate exchange over peer memory (P:381's one process per
+ * GPU).  The shard's merge kernel stores its N x k keys straight into every rank's
+ * inbox (NVLink stores through CUDA IPC mappings) and releases a per-batch flag; each
+ * rank's tail acquires the world flags and reads its own inbox -- no all-gather call.
+ * Inbox slots alternate by batch parity and a sender waits (normally not at all) until
+ * the receiver has consumed the batch that used the slot two batches earlier.  A peer
+ * that does not deliver within 5 s fails the call with ARGUS_E_NCCL instead of hanging.
+ * NCCL mode: set up by argus_route_init itself (IPC handles exchanged over the
+ * communicator); if any rank cannot map its peers, every rank keeps ncclAllGather
+ * (ARGUS_NO_P2P=1 forces that).  External mode (world > 1, no unique id): the caller
+ * connects the ranks -- every rank calls argus_p2p_export (64-byte handle out), the
+ * caller exchanges the handles (e.g. torch.distributed all_gather_object), and every
+ * rank calls argus_p2p_connect with the [world][64] array in rank order.  Afterwards
+ * argus_route_batch* work in external mode as collectives (every rank passes the same
+ * prompts and quotas; no broadcast).  Errors: ARGUS_E_INVALID (not external mode, k = 0,
+ * world > 16, connect before export), ARGUS_E_CUDA (a handle that cannot be mapped). */
+int argus_p2p_export(argus_router* r, void* handle_out);
+int argus_p2p_connect(argus_router* r, const void* handles);
+
 /* Make `stream` (cudaStream_t; NULL = the router's stream) wait, on the device,
  * for all routing work enqueued so far, including pipelined tails.  No host
  * synchronisation.  Errors: ARGUS_E_CUDA. */

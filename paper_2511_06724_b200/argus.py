@@ -35,7 +35,7 @@ SYMBOLS = (
     "argus_strerror", "argus_solve_allocation", "argus_oda_pasm", "argus_pasm_degradation", "argus_set_policy",
     "argus_affinity_histogram", "argus_set_workers", "argus_get_queues", "argus_route_batch_ex",
     "argus_route_batch_ex_dev", "argus_cache_insert_h", "argus_route_batch_async", "argus_route_wait",
-    "argus_debug_capture",
+    "argus_debug_capture", "argus_p2p_export", "argus_p2p_connect",
 )
 STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
@@ -101,6 +101,8 @@ def _load():
         "argus_route_batch_async": [P, P, I32, P, P, P, P, P, P, P],
         "argus_route_wait": [P, I64],
         "argus_debug_capture": [P, P, I64],
+        "argus_p2p_export": [P, P],
+        "argus_p2p_connect": [P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -397,6 +399,17 @@ class Router:
         ld = int(scores_dev.shape[-1]) if ld is None else int(ld)
         self._dbg_keep = scores_dev
         _check(_lib.argus_debug_capture(self._h, _p(scores_dev), ld), "argus_debug_capture")
+
+    def argus_p2p_export(self) -> bytes:
+        """External mode: this rank's 64-byte inbox handle (to be exchanged by the caller)."""
+        buf = C.create_string_buffer(64)
+        _check(_lib.argus_p2p_export(self._h, buf), "argus_p2p_export")
+        return buf.raw
+
+    def argus_p2p_connect(self, handles):
+        """External mode: map every rank's inbox (handles: list of 64-byte handles in rank order)."""
+        blob = C.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * len(handles))
+        _check(_lib.argus_p2p_connect(self._h, blob), "argus_p2p_connect")
 
     def argus_profile_enable(self, on=True):
         _check(_lib.argus_profile_enable(self._h, int(bool(on))), "argus_profile_enable")

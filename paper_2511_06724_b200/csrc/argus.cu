@@ -174,6 +174,14 @@ struct argus_router {
   int16_t* d_wlist = nullptr;      // [32][32]
   int32_t* d_wcount = nullptr;     // [32]
   int32_t* d_quota[2] = {nullptr, nullptr};  // [32] quotas broadcast from rank 0 (NCCL mode), per parity
+  // fused C-2 over peer memory (k_merge_send): this rank's inbox [header | keys [2][G][max_batch][k]]
+  // exported by CUDA IPC; peers' inboxes mapped into this process
+  bool p2p = false;
+  uint8_t* d_inbox = nullptr;
+  uint8_t* peer_inbox[P2P_MAX] = {};  // [world] (own inbox at [rank])
+  bool peer_opened[P2P_MAX] = {};
+  uint32_t p2p_seq = 0;               // batches exchanged so far (identical on every rank)
+  int32_t* d_p2p_ticket = nullptr;
   // pipelined NCCL mode: every collective on one stream in program order (identical on all
   // ranks), and the all-gather + tail of batch b deferred until call b+1 has issued its
   // broadcast, so the comm stream runs bcast(b+1) before AG(b) and the scans run back to back
@@ -195,6 +203,7 @@ struct argus_router {
     uint32_t* flags = nullptr;
     int async_slot = -1;  // argus_route_batch_async slot whose result copy follows the tail
     size_t async_bytes = 0;
+    uint32_t seq = 0;     // fused exchange: the batch's sequence number
   } def;
   float* d_wtime = nullptr;        // [MAX_WORKERS]
   int32_t* d_queue = nullptr;      // [MAX_WORKERS]
@@ -220,6 +229,80 @@ struct argus_router {
 };
 
 constexpr int MAX_WORKERS = 1024;
+
+// ------------------------------------------------------------------ fused exchange inboxes
+// Inbox of one rank (bytes): [arrival flags: 2 parities x P2P_MAX senders u32][consumed: 2 u32]
+// padded to 256, then keys [2 parities][world][max_batch][k] u64.  Parity = batch sequence & 1.
+constexpr size_t INBOX_HDR = 256;
+static size_t inbox_bytes(const argus_router* r) {
+  return INBOX_HDR + sizeof(uint64_t) * 2 * (size_t)r->cfg.world * r->cfg.max_batch * r->cfg.k;
+}
+static uint64_t* inbox_keys(const argus_router* r, uint8_t* base, int par) {
+  return reinterpret_cast<uint64_t*>(base + INBOX_HDR) + (size_t)par * r->cfg.world * r->cfg.max_batch * r->cfg.k;
+}
+static uint32_t* inbox_flags(uint8_t* base, int par) { return reinterpret_cast<uint32_t*>(base) + par * P2P_MAX; }
+static uint32_t* inbox_consumed(uint8_t* base, int par) {
+  return reinterpret_cast<uint32_t*>(base) + 2 * P2P_MAX + par;
+}
+
+static P2PSend p2p_send_args(argus_router* r, uint32_t seq) {
+  P2PSend a{};
+  const int par = (int)(seq & 1u);
+  a.G = r->cfg.world;
+  a.rank = r->cfg.rank;
+  a.seq = seq;
+  for (int g = 0; g < a.G; ++g) {
+    a.keys[g] = inbox_keys(r, r->peer_inbox[g], par);
+    a.flag[g] = inbox_flags(r->peer_inbox[g], par) + r->cfg.rank;
+    a.consumed[g] = inbox_consumed(r->peer_inbox[g], par);
+  }
+  a.err = r->flags_cur ? r->flags_cur : r->d_flags;
+  return a;
+}
+
+static int p2p_alloc(argus_router* r) {
+  if (r->d_inbox) return ARGUS_OK;
+  if (cudaMalloc((void**)&r->d_inbox, inbox_bytes(r)) != cudaSuccess ||
+      cudaMemset(r->d_inbox, 0, inbox_bytes(r)) != cudaSuccess ||
+      cudaMalloc((void**)&r->d_p2p_ticket, sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(r->d_p2p_ticket, 0, sizeof(int32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return ARGUS_E_CUDA;
+  }
+  r->peer_inbox[r->cfg.rank] = r->d_inbox;
+  return ARGUS_OK;
+}
+
+// map every other rank's inbox (64-byte cudaIpcMemHandle_t each, [world])
+static int p2p_open(argus_router* r, const uint8_t* handles) {
+  for (int g = 0; g < r->cfg.world; ++g) {
+    if (g == r->cfg.rank || r->peer_opened[g]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * g, sizeof(h));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return ARGUS_E_CUDA;
+    }
+    r->peer_inbox[g] = static_cast<uint8_t*>(p);
+    r->peer_opened[g] = true;
+  }
+  return ARGUS_OK;
+}
+
+static void p2p_close(argus_router* r) {
+  for (int g = 0; g < P2P_MAX; ++g)
+    if (r->peer_opened[g]) {
+      cudaIpcCloseMemHandle(r->peer_inbox[g]);
+      r->peer_opened[g] = false;
+      r->peer_inbox[g] = nullptr;
+    }
+  if (r->d_inbox) cudaFree(r->d_inbox);
+  if (r->d_p2p_ticket) cudaFree(r->d_p2p_ticket);
+  r->d_inbox = nullptr;
+  r->d_p2p_ticket = nullptr;
+  r->p2p = false;
+}
 
 // ------------------------------------------------------------------ helpers
 #define CU_TRY(r, expr)                                               \
@@ -366,6 +449,31 @@ int argus_debug_capture(argus_router* r, float* scores_dev, int64_t ld) {
   return ARGUS_OK;
 }
 
+int argus_p2p_export(argus_router* r, void* handle_out) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (!handle_out || r->cfg.world < 2 || r->comm || r->cfg.k == 0 || r->cfg.world > P2P_MAX) return ARGUS_E_INVALID;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = p2p_alloc(r);
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  CU_TRY(r, cudaIpcGetMemHandle(&h, r->d_inbox));
+  memset(handle_out, 0, 64);
+  memcpy(handle_out, &h, sizeof(h));
+  return ARGUS_OK;
+}
+
+int argus_p2p_connect(argus_router* r, const void* handles) {
+  int rc = check_state(r);
+  if (rc) return rc;
+  if (!handles || r->cfg.world < 2 || r->comm || !r->d_inbox) return ARGUS_E_INVALID;
+  CU_TRY(r, cudaSetDevice(r->cfg.device));
+  rc = p2p_open(r, static_cast<const uint8_t*>(handles));
+  if (rc) return rc;
+  r->p2p = true;
+  return ARGUS_OK;
+}
+
 int argus_profile_enable(argus_router* r, int on) {
   if (!r) return ARGUS_E_INVALID;
   cudaSetDevice(r->cfg.device);
@@ -476,6 +584,7 @@ int argus_route_destroy(argus_router* r) {
   if (r->d_outblk) cudaFree(r->d_outblk);
   for (auto& x : r->ev_open) { cudaEventDestroy(x.second.first); cudaEventDestroy(x.second.second); }
   for (auto e : r->ev_pool) cudaEventDestroy(e);
+  p2p_close(r);
   if (r->comm) nccl().CommDestroy(r->comm);
   for (int q = 0; q < 2; ++q)
     for (cudaEvent_t e : {r->ev_in[q], r->ev_prep[q], r->ev_scan[q], r->ev_tail[q], r->ev_bcast[q], r->ev_ag[q]})
@@ -731,6 +840,44 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     return ARGUS_E_CUDA;
   }
   cleanup_tmp();
+  // NCCL mode: the fused exchange over peer memory replaces the all-gather when every rank
+  // can map every other rank's inbox (all ranks decide together: a MIN all-reduce)
+  if (nccl_mode(r) && k > 0 && G <= P2P_MAX && !getenv("ARGUS_NO_P2P")) {
+    int ok = p2p_alloc(r) == ARGUS_OK;
+    uint8_t* d_h = nullptr;
+    int32_t* d_ok = nullptr;
+    std::vector<uint8_t> hh(64 * (size_t)G, 0);
+    if (cudaMalloc((void**)&d_h, hh.size()) != cudaSuccess || cudaMalloc((void**)&d_ok, 4) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(d_h);
+      argus_route_destroy(r);
+      return ARGUS_E_CUDA;
+    }
+    cudaIpcMemHandle_t h{};
+    if (ok && G > 1) ok = cudaIpcGetMemHandle(&h, r->d_inbox) == cudaSuccess;
+    memcpy(hh.data() + 64 * (size_t)c.rank, &h, sizeof(h));
+    bool nc = cudaMemcpy(d_h, hh.data(), hh.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+              nccl().AllGather(d_h + 64 * (size_t)c.rank, d_h, 64, ncclUint8, r->comm, r->stream) == ncclSuccess &&
+              cudaMemcpy(hh.data(), d_h, hh.size(), cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (nc && ok) ok = p2p_open(r, hh.data()) == ARGUS_OK;
+    int32_t okv = ok ? 1 : 0;
+    nc = nc && cudaMemcpy(d_ok, &okv, 4, cudaMemcpyHostToDevice) == cudaSuccess &&
+         nccl().AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, r->comm, r->stream) == ncclSuccess &&
+         cudaMemcpy(&okv, d_ok, 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d_h);
+    cudaFree(d_ok);
+    cudaGetLastError();
+    if (!nc) {
+      argus_route_destroy(r);
+      return ARGUS_E_NCCL;
+    }
+    if (okv) {
+      r->p2p = true;
+    } else {
+      p2p_close(r);  // some rank cannot map its peers: every rank keeps the NCCL all-gather
+      if (getenv("ARGUS_DEBUG")) fprintf(stderr, "argus: fused peer exchange unavailable, using ncclAllGather\n");
+    }
+  }
 #undef TRY_RC
   *out = r;
   return ARGUS_OK;
@@ -871,7 +1018,7 @@ static int64_t ring_head(const argus_router* r) {
 // the C-1 broadcast; the tail then reads them from there.
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
                         int q, cudaStream_t s_prep = nullptr, cudaStream_t s_scan = nullptr,
-                        bool quota_bcast = false, const int32_t* quota = nullptr);
+                        bool quota_bcast = false, const int32_t* quota = nullptr, uint32_t send_seq = 0);
 
 int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev) {
   if (!keys_dev) return ARGUS_E_INVALID;
@@ -884,7 +1031,8 @@ int argus_route_partial_dev(argus_router* r, const float* prompts_dev, int32_t N
 // With s_prep / s_scan (pipelined mode) prep and scan go to those streams, without
 // the programmatic (PDL) relaxation, and the caller inserts the events between them.
 static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, uint64_t* keys_dev, int32_t* P_out,
-                        int q, cudaStream_t s_prep, cudaStream_t s_scan, bool quota_bcast, const int32_t* quota) {
+                        int q, cudaStream_t s_prep, cudaStream_t s_scan, bool quota_bcast, const int32_t* quota,
+                        uint32_t send_seq) {
   const bool pipelined = s_prep != nullptr;
   if (!s_prep) s_prep = r->stream;
   if (!s_scan) s_scan = r->stream;
@@ -1009,6 +1157,12 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
       launch_merge_topk(r->d_partial[q], a.P, N, k, keys_dev, nullptr, nullptr, s_scan);
     }
     LAUNCHED(r);
+  } else if (send_seq) {  // K5 + C-2 fused: merged keys stored into every rank's inbox
+    {
+      StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL, s_scan);
+      launch_merge_send(r->d_partial[q], a.P, N, k, p2p_send_args(r, send_seq), r->d_p2p_ticket, s_scan, !pipelined);
+    }
+    LAUNCHED(r);
   }
   return ARGUS_OK;
 }
@@ -1017,7 +1171,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
                        uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex = nullptr,
-                       int q = -1);
+                       int q = -1, uint32_t p2p_seq = 0);
 static int flush_deferred(argus_router* r);
 static int async_harvest(argus_router* r, int q);
 // route_batch* in NCCL mode: the quotas are rank 0's (broadcast), other ranks may pass NULL
@@ -1046,8 +1200,10 @@ int argus_route_finish_dev(argus_router* r, const uint64_t* keys_all_dev, int32_
 
 static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int32_t N, const int32_t* quota,
                        int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev, float* quality_dev,
-                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex, int q) {
+                       uint8_t* status_dev, cudaStream_t s, bool pdl, const argus_route_extra* ex, int q,
+                       uint32_t p2p_seq) {
   if (q < 0) q = r->cur;  // the parity of the buffers this batch's partial_impl used
+  if (p2p_seq) keys_in = inbox_keys(r, r->d_inbox, (int)(p2p_seq & 1u));  // filled by the fused exchange
   const bool qdev = r->quota_dev_next;  // consumed by this call whatever happens
   r->quota_dev_next = false;
   int rc = check_state(r);
@@ -1060,6 +1216,11 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   TailArgs m{};
   m.keys_in = keys_in;
   m.P = P;
+  if (p2p_seq) {
+    m.p2p_flags = inbox_flags(r->d_inbox, (int)(p2p_seq & 1u));
+    m.p2p_consumed = inbox_consumed(r->d_inbox, (int)(p2p_seq & 1u));
+    m.p2p_seq = p2p_seq;
+  }
   m.topk_idx = topk_idx_dev ? topk_idx_dev : r->d_idx;
   m.topk_score = topk_score_dev ? topk_score_dev : r->d_score;
   m.Xb = r->d_Xb[q];  // the bf16 copy of this batch made by partial_impl
@@ -1139,7 +1300,7 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
                              float* quality_dev, uint8_t* status_dev, const argus_route_extra* ex) {
   int rc = check_state(r);
   if (rc) return rc;
-  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;  // external mode: use partial/finish
+  if (r->cfg.world > 1 && !r->comm && !r->p2p) return ARGUS_E_STATE;  // external mode: partial/finish
   if (N < 1 || N > r->cfg.max_batch || !quota_ok(r, quota) || !option_out_dev ||
       (r->cfg.k > 0 && (!topk_idx_dev || !topk_score_dev)))
     return ARGUS_E_INVALID;
@@ -1156,8 +1317,9 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_in[q], 0));
     if (r->tail_inflight[q]) CU_TRY(r, cudaStreamWaitEvent(r->prep_stream, r->ev_tail[q], 0));  // parity q free
     const bool qb = quota_from_root(r);
-    rc = partial_impl(r, prompts_dev, N, r->cfg.k > 0 ? r->d_keys[q] : nullptr, &P, q, r->prep_stream,
-                      r->scan_stream, qb, quota);
+    const uint32_t seq = r->p2p ? ++r->p2p_seq : 0u;  // fused exchange instead of the all-gather
+    rc = partial_impl(r, prompts_dev, N, (r->cfg.k > 0 && !seq) ? r->d_keys[q] : nullptr, &P, q, r->prep_stream,
+                      r->scan_stream, qb, quota, seq);
     if (rc) return rc;
     CU_TRY(r, cudaEventRecord(r->ev_scan[q], r->scan_stream));
     rc = flush_deferred(r);
@@ -1178,6 +1340,7 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     if (ex) D.ex = *ex;
     D.flags = r->flags_cur;
     D.async_slot = -1;
+    D.seq = seq;
     r->seq++;
     return ARGUS_OK;
   }
@@ -1197,6 +1360,15 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
     r->tail_inflight[q] = true;
     r->seq++;
     return ARGUS_OK;
+  }
+  if (r->p2p) {  // NCCL mode or external mode with mapped inboxes: the fused exchange
+    const bool qb = quota_from_root(r);
+    const uint32_t seq = ++r->p2p_seq;
+    rc = partial_impl(r, prompts_dev, N, nullptr, &P, 0, nullptr, nullptr, qb, quota, seq);
+    if (rc) return rc;
+    r->quota_dev_next = qb;
+    return finish_impl(r, nullptr, r->cfg.world, N, quota, option_out_dev, topk_idx_dev, topk_score_dev,
+                       quality_dev, status_dev, r->stream, true, ex, -1, seq);
   }
   if (!nccl_mode(r)) {  // single shard: the tail merges the per-CTA lists directly
     rc = partial_impl(r, prompts_dev, N, nullptr, &P, 0);
@@ -1222,7 +1394,9 @@ static int flush_deferred(argus_router* r) {
   if (!D.valid) return ARGUS_OK;
   D.valid = false;
   const int q = D.q, k = r->cfg.k;
-  if (k > 0) {
+  if (D.seq) {  // fused exchange: the tail itself waits for the peers' keys
+    CU_TRY(r, cudaStreamWaitEvent(r->tail_stream, r->ev_scan[q], 0));
+  } else if (k > 0) {
     CU_TRY(r, cudaStreamWaitEvent(r->comm_stream, r->ev_scan[q], 0));
     NC_TRY(r, nccl().AllGather(r->d_keys[q], r->d_keys_all[q], (size_t)D.N * k, ncclUint64, r->comm,
                                r->comm_stream));
@@ -1235,7 +1409,7 @@ static int flush_deferred(argus_router* r) {
   r->flags_cur = D.flags;
   r->quota_dev_next = D.qdev;
   int rc = finish_impl(r, r->d_keys_all[q], r->cfg.world, D.N, D.quota, D.option, D.idx, D.score, D.quality,
-                       D.status, r->tail_stream, false, D.has_ex ? &D.ex : nullptr, q);
+                       D.status, r->tail_stream, false, D.has_ex ? &D.ex : nullptr, q, D.seq);
   r->flags_cur = saved;
   if (rc) return rc;
   CU_TRY(r, cudaEventRecord(r->ev_tail[q], r->tail_stream));
@@ -1288,6 +1462,10 @@ int argus_sync(argus_router* r) {
   }
   r->pending = false;
   const uint32_t fl = *r->h_flags;
+  if (fl & FLAG_PEER_TIMEOUT) {  // a peer never delivered its keys: the exchange is broken
+    r->poisoned = true;
+    return ARGUS_E_NCCL;
+  }
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
   return ARGUS_OK;
@@ -1313,7 +1491,7 @@ int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const
   int32_t* worker_out = extra ? extra->worker : nullptr;
   uint64_t* handle_out = extra ? extra->topk_handle : nullptr;
   if (root && !prompts) return ARGUS_E_INVALID;
-  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
+  if (r->cfg.world > 1 && !r->comm && !r->p2p) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
   if (r->pending) {  // drain earlier async work and clear its deferred flags
@@ -1359,6 +1537,10 @@ int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const
   if (worker_out) memcpy(worker_out, Hb + o_wk, 4 * (size_t)N);
   uint32_t fl;
   memcpy(&fl, Hb, 4);
+  if (fl & FLAG_PEER_TIMEOUT) {
+    r->poisoned = true;
+    return ARGUS_E_NCCL;
+  }
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
   return ARGUS_OK;
@@ -1366,6 +1548,7 @@ int argus_route_batch_ex(argus_router* r, const float* prompts, int32_t N, const
 
 // ------------------------------------------------------------------ asynchronous host-buffer calls
 static int flags_rc(uint32_t fl) {
+  if (fl & FLAG_PEER_TIMEOUT) return ARGUS_E_NCCL;
   if (fl & FLAG_INVALID_INPUT) return ARGUS_E_INVALID;
   if (fl & FLAG_OVERFLOW) return ARGUS_W_OVERFLOW;
   return ARGUS_OK;
@@ -1410,7 +1593,7 @@ int argus_route_batch_async(argus_router* r, const float* prompts, int32_t N, co
       (r->cfg.k > 0 && (!topk_idx || !topk_score)))
     return ARGUS_E_INVALID;
   if (root && !prompts) return ARGUS_E_INVALID;
-  if (r->cfg.world > 1 && !r->comm) return ARGUS_E_STATE;
+  if (r->cfg.world > 1 && !r->comm && !r->p2p) return ARGUS_E_STATE;
   CU_TRY(r, cudaSetDevice(r->cfg.device));
   const int d = r->cfg.d, k = r->cfg.k, L = r->cfg.L;
   const int q = (int)(r->next_ticket % argus_router::NASYNC);

@@ -71,4 +71,108 @@ void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint
     launch_pdl(k_merge_topk<8>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, keys_out, idx_out, score_out);
 }
 
+
+// ------------------------------------------------------------------ K5 + C-2 fused over peer memory
+// The shard's merge of its P per-range lists, with the exchange step folded in: each
+// prompt's k merged keys are stored straight into slot [rank] of every rank's inbox
+// (NVLink peer stores through CUDA IPC mappings; the own inbox is local memory), and
+// the launch's last CTA, after a system-scope fence, publishes the batch sequence
+// number in every inbox's flag word [rank] with a release store.  The receivers' tails
+// acquire the G flags before reading their inbox (one exchange of N*k
+// keys per batch, here without an NCCL call or a separate kernel).  Inbox slots are
+// double-buffered by batch parity; before storing into a peer's slot, each CTA waits
+// (one acquire load per peer, normally already satisfied) until that peer's tail has
+// consumed the batch that used the slot two batches ago, so no rank can overwrite keys
+// a slower rank has not read yet, whatever the collectives' buffering lets run ahead.
+namespace {
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+}  // namespace
+
+template <int KMAX>
+__global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t* __restrict__ in, int P, int N, int k,
+                                                                P2PSend dst, int* ticket) {
+  const int i = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ uint64_t wl[MERGE_WARPS][KMAX];
+  __shared__ int is_last;
+  pdl_wait();
+  if (threadIdx.x < dst.G && dst.seq > 2) {  // credit: peer's slot of this parity is free again
+    const uint64_t t0 = gtime();
+    while (ld_acquire_sys(dst.consumed[threadIdx.x]) + 2 < dst.seq) {
+      __nanosleep(200);
+      if (gtime() - t0 > P2P_TIMEOUT_NS) {
+        atomicOr(dst.err, FLAG_PEER_TIMEOUT);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  TopList<KMAX> l;
+  l.clear();
+  const int total = P * k;
+  const int per = (total + MERGE_WARPS - 1) / MERGE_WARPS;
+  const int e0 = warp * per, e1 = min(total, e0 + per);
+  constexpr int B = 8;
+  for (int e = e0 + lane; e < e1; e += 32 * B) {
+    uint64_t buf[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int ee = e + u * 32;
+      uint64_t key = 0;
+      if (ee < e1) {
+        const int p = ee / k, t = ee - p * k;
+        key = __ldg(reinterpret_cast<const unsigned long long*>(in) + ((int64_t)p * N + i) * k + t);
+      }
+      buf[u] = key;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) l.insert(buf[u]);
+  }
+  warp_merge_topk<KMAX>(l, k, wl[warp]);
+  __syncthreads();
+  if (warp == 0) {
+    TopList<KMAX> m;
+    m.clear();
+    if (lane < MERGE_WARPS * k) m.insert(wl[lane / k][lane % k]);
+    __shared__ uint64_t out_s[KMAX];
+    warp_merge_topk<KMAX>(m, k, out_s);
+    __syncwarp();
+    // lane (g, t): key t of this prompt into inbox g, slot [rank][i]
+    for (int x = lane; x < dst.G * k; x += 32) {
+      const int g = x / k, t = x - g * k;
+      dst.keys[g][((int64_t)dst.rank * N + i) * k + t] = out_s[t];
+    }
+  }
+  __threadfence_system();  // this CTA's peer stores before its ticket
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  pdl_launch();
+  if (is_last && threadIdx.x < dst.G) {
+    __threadfence_system();
+    st_release_sys(dst.flag[threadIdx.x], dst.seq);
+    if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+  }
+}
+
+void launch_merge_send(const uint64_t* in, int32_t P, int32_t N, int32_t k, const P2PSend& dst, int* ticket,
+                       cudaStream_t s, bool pdl) {
+  if (k <= 4)
+    launch_pdl_opt(pdl, k_merge_send<4>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
+  else
+    launch_pdl_opt(pdl, k_merge_send<8>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
+}
+
 }  // namespace argus

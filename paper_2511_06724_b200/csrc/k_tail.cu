@@ -46,6 +46,15 @@ __shared__ unsigned long long tail_ts[24];  // 20: clock64 at entry
     if (ARGUS_TAIL_TIMING && threadIdx.x == 0) tail_ts[i] = gtimer(); \
   } while (0)
 
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -495,6 +504,21 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   };
   load_w1(blockIdx.y);
   pdl_wait();
+  if (a.p2p_flags != nullptr) {
+    // fused exchange (k_merge_send): the P ranks' keys are in this rank's inbox once their
+    // flags carry this batch's sequence number (acquire; the senders fenced at sys scope)
+    if (tid < a.P) {
+      const uint64_t t0 = gtimer();
+      while (ld_acquire_sys(a.p2p_flags + tid) < a.p2p_seq) {
+        __nanosleep(100);
+        if (gtimer() - t0 > P2P_TIMEOUT_NS) {
+          atomicOr(a.flags, FLAG_PEER_TIMEOUT);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
   TS(1);
   // inverse norms of this warp's phase-2 prompts (0 marks an invalid prompt)
   float iq_r[PB / TW];
@@ -792,6 +816,8 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   if (!is_last) return;
   __threadfence();
   if (tid == 0) *a.launch_cnt = 0;
+  // every CTA of the launch has staged its inbox keys: the senders may reuse the slot
+  if (a.p2p_consumed != nullptr && tid == 0) st_release_sys(a.p2p_consumed, a.p2p_seq);
   TS(10);
   if (a.policy == 0) assign_all(a, smraw);
   if (a.n_workers > 0) {

@@ -31,7 +31,8 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 // error flags written by kernels into a device word (bitwise OR)
-enum : uint32_t { FLAG_INVALID_INPUT = 1u, FLAG_OVERFLOW = 2u };
+enum : uint32_t { FLAG_INVALID_INPUT = 1u, FLAG_OVERFLOW = 2u, FLAG_PEER_TIMEOUT = 4u };
+constexpr uint64_t P2P_TIMEOUT_NS = 5000000000ull;  // a peer that does not deliver in 5 s: error, no hang
 
 struct ScanArgs {
   const __nv_bfloat16* Xb;   // [n_pad][d] bf16 prompts (rows >= N are zero)
@@ -96,10 +97,28 @@ cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, con
 void launch_merge_topk(const uint64_t* in, int32_t P, int32_t N, int32_t k, uint64_t* keys_out,
                        uint32_t* idx_out, float* score_out, cudaStream_t s);
 
+// K5 + C-2 fused (k_merge.cu): peer inboxes of one parity.  keys[g] = base of rank g's
+// inbox keys [G][max_batch][k] (IPC-mapped for g != rank), flag[g] = rank g's flag word
+// for senders [rank] (the release store of the batch sequence number).
+constexpr int P2P_MAX = 16;
+struct P2PSend {
+  uint64_t* keys[P2P_MAX];            // rank g's inbox keys of this parity
+  uint32_t* flag[P2P_MAX];            // rank g's arrival flag [parity][sender = rank]
+  const uint32_t* consumed[P2P_MAX];  // rank g's consumed counter of this parity
+  uint32_t* err;                      // this rank's flags word (FLAG_PEER_TIMEOUT)
+  int32_t G, rank;
+  uint32_t seq;
+};
+void launch_merge_send(const uint64_t* in, int32_t P, int32_t N, int32_t k, const P2PSend& dst, int* ticket,
+                       cudaStream_t s, bool pdl);
+
 struct TailArgs {
   // phase M: candidate lists -> final top-k
   const uint64_t* keys_in;   // [P][N][k] candidate keys (per-range partials, or all-gathered shards)
   int32_t P;
+  const uint32_t* p2p_flags; // [P] or nullptr: keys_in is this rank's inbox, filled by the P ranks'
+  uint32_t p2p_seq;          // merge kernels; wait until every flag >= p2p_seq (acquire, sys scope)
+  uint32_t* p2p_consumed;    // this rank's consumed counter of the parity: p2p_seq once staged
   uint32_t* topk_idx;        // [N][k] out: global id = id_base + age index of the key
   float* topk_score;         // [N][k] out
   uint32_t id_base;          // global id of the oldest live entry

@@ -365,6 +365,17 @@ int argus_route_batch_ex_dev(argus_router* r, const float* prompts_dev, int32_t 
                              int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
                              float* quality_dev, uint8_t* status_dev, const argus_route_extra* extra);
 
+/* argus_route_batch_ex_dev for prompts already in bf16 (SURVEY §8(b) "prompts_bf16_dev";
+ * e.g. CLIP embeddings kept in bf16 by the caller): prompts_bf16_dev is device bf16 [N][d]
+ * row-major, 4-byte aligned.  The rows enter the scan as they are; their inverse norms
+ * are computed from the same values in the same order as the fp32 path computes them
+ * after rounding, so a batch gives bit-identical outputs through either call when its
+ * fp32 values round to these bf16 values.  Non-finite or zero rows: ARGUS_E_INVALID
+ * (reported by argus_sync like the fp32 device call). */
+int argus_route_batch_bf16_dev(argus_router* r, const void* prompts_bf16_dev, int32_t N, const int32_t* quota,
+                               int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
+                               float* quality_dev, uint8_t* status_dev, const argus_route_extra* extra);
+
 /* Cache lifecycle ("Each prompt stores intermediate states at K"): append n
  * entries like argus_cache_insert and store handles [n] (u64, caller-defined, e.g.
  * an object-store key of the 144 KB intermediate state; NULL = 0) with them.

@@ -35,7 +35,7 @@ SYMBOLS = (
     "argus_strerror", "argus_solve_allocation", "argus_oda_pasm", "argus_pasm_degradation", "argus_set_policy",
     "argus_affinity_histogram", "argus_set_workers", "argus_get_queues", "argus_route_batch_ex",
     "argus_route_batch_ex_dev", "argus_cache_insert_h", "argus_route_batch_async", "argus_route_wait",
-    "argus_debug_capture", "argus_p2p_export", "argus_p2p_connect",
+    "argus_debug_capture", "argus_p2p_export", "argus_p2p_connect", "argus_route_batch_bf16_dev",
 )
 STAGES = ("prep", "scan", "merge_local", "unused3", "tail", "unused5", "insert")
 
@@ -102,6 +102,7 @@ def _load():
         "argus_route_wait": [P, I64],
         "argus_debug_capture": [P, P, I64],
         "argus_p2p_export": [P, P],
+        "argus_route_batch_bf16_dev": [P, P, I32, P, P, P, P, P, P, P],
         "argus_p2p_connect": [P, P],
     }
     for name, args in sig.items():
@@ -323,6 +324,16 @@ class Router:
         return _check(_lib.argus_route_batch_ex_dev(self._h, _p(prompts_dev), N, _p(quota), _p(option),
                                                     _p(topk_idx), _p(topk_score), _p(quality), _p(status),
                                                     C.byref(ex)), "argus_route_batch_ex_dev")
+
+    def argus_route_batch_bf16_dev(self, prompts_bf16_dev, quota, option, topk_idx, topk_score, quality=None,
+                                   status=None, optimal=None, worker=None, topk_handle=None, N=None):
+        """Device route with bf16 prompts [N][d] (a torch.bfloat16 CUDA tensor)."""
+        quota = None if quota is None else np.ascontiguousarray(quota, np.int32)
+        N = int(prompts_bf16_dev.shape[0]) if N is None else int(N)
+        ex = argus_route_extra(_p(optimal), _p(worker), _p(topk_handle))
+        return _check(_lib.argus_route_batch_bf16_dev(self._h, _p(prompts_bf16_dev), N, _p(quota), _p(option),
+                                                      _p(topk_idx), _p(topk_score), _p(quality), _p(status),
+                                                      C.byref(ex)), "argus_route_batch_bf16_dev")
 
     def argus_route_batch_async(self, prompts, quota, out, N=None):
         """Enqueue one batch from (pinned) host memory; outputs land in the arrays of

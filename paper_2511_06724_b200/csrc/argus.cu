@@ -217,6 +217,7 @@ struct argus_router {
   int scan_reserve = 2;            // pipelined one-slice scans: SMs left to prep / tail (ARGUS_SCAN_RESERVE)
   bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
+  bool prompts_bf16 = false;       // the current call's device prompts are bf16 (argus_route_batch_bf16_dev)
   // argus_debug_capture (parity test T2): the scan also writes every exact score here
   float* dbg_scores = nullptr;
   int64_t dbg_ld = 0;
@@ -1048,7 +1049,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // K6 on the root (or everywhere in external mode), then C-1 broadcast of the bf16 batch
   if (root) {
     StageScope sc(r, ARGUS_STAGE_PREP, s_prep);
-    launch_prep_queries(prompts_dev, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q],
+    launch_prep_queries(prompts_dev, r->prompts_bf16, N, n_pad, d, r->d_Xb[q], r->d_invq[q], r->d_gthr[q], r->d_ctr[q],
                         r->flags_cur ? r->flags_cur : r->d_flags,
                         s_prep, !pipelined, quota_bcast ? quota : nullptr, r->cfg.L, r->d_quota[q]);
     LAUNCHED(r);
@@ -1422,6 +1423,17 @@ static int flush_deferred(argus_router* r) {
     CU_TRY(r, cudaEventRecord(r->ev_async[a], r->d2h_stream));
   }
   return ARGUS_OK;
+}
+
+int argus_route_batch_bf16_dev(argus_router* r, const void* prompts_bf16_dev, int32_t N, const int32_t* quota,
+                               int32_t* option_out_dev, uint32_t* topk_idx_dev, float* topk_score_dev,
+                               float* quality_dev, uint8_t* status_dev, const argus_route_extra* extra) {
+  if (!r) return ARGUS_E_INVALID;
+  r->prompts_bf16 = true;  // K6 copies the rows as they are (same norm, same validity checks)
+  const int rc = argus_route_batch_ex_dev(r, static_cast<const float*>(prompts_bf16_dev), N, quota, option_out_dev,
+                                          topk_idx_dev, topk_score_dev, quality_dev, status_dev, extra);
+  r->prompts_bf16 = false;
+  return rc;
 }
 
 int argus_route_join(argus_router* r, void* stream) {

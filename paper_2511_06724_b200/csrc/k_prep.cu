@@ -32,6 +32,29 @@ __device__ __forceinline__ float row_to_bf16(const float* __restrict__ src, __nv
   return acc;
 }
 
+// The same for a row that is already bf16 (argus_route_batch_bf16_dev): copied as is, the
+// norm from the same values in the same order, so inv_q is bit-identical to what the fp32
+// path computes for inputs that round to these bf16 values.
+__device__ __forceinline__ float row_bf16(const __nv_bfloat162* __restrict__ src, __nv_bfloat162* dst, int d,
+                                          bool* bad) {
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  bool b = false;
+  for (int j = lane; j < d / 2; j += 32) {
+    const __nv_bfloat162 h = src[j];
+    const float2 r = __bfloat1622float2(h);
+    b |= !isfinite(r.x) || !isfinite(r.y);
+    acc = __fmaf_rn(r.x, r.x, acc);
+    acc = __fmaf_rn(r.y, r.y, acc);
+    dst[j] = h;
+  }
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, m));
+  b = __any_sync(0xffffffffu, b);
+  *bad = b || !(acc > 0.f) || !isfinite(acc);
+  return acc;
+}
+
 __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t g0, int d,
                               int rank, int world, int64_t cap, int dry, __nv_bfloat16* __restrict__ Cb,
                               float* __restrict__ inv_c, uint32_t* flags) {
@@ -53,7 +76,7 @@ __global__ void k_insert_rows(const float* __restrict__ rows, int64_t n, int64_t
   }
 }
 
-__global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, int d,
+__global__ void k_prep_queries(const void* __restrict__ X, int in_bf16, int N, int n_pad, int d,
                                __nv_bfloat16* __restrict__ Xb, float* __restrict__ inv_q,
                                uint64_t* __restrict__ gthr, int32_t* __restrict__ ctr, uint32_t* flags,
                                QuotaVec quota, int32_t* __restrict__ quota_dev) {
@@ -72,8 +95,9 @@ __global__ void k_prep_queries(const float* __restrict__ X, int N, int n_pad, in
     return;
   }
   bool bad;
-  float ss = row_to_bf16(X + (int64_t)warp * d, reinterpret_cast<__nv_bfloat162*>(Xb + (int64_t)warp * d),
-                         d, &bad);
+  __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(Xb + (int64_t)warp * d);
+  const float ss = in_bf16 ? row_bf16(reinterpret_cast<const __nv_bfloat162*>(X) + (int64_t)warp * d / 2, dst, d, &bad)
+                           : row_to_bf16(reinterpret_cast<const float*>(X) + (int64_t)warp * d, dst, d, &bad);
   if (lane == 0) {
     inv_q[warp] = bad ? 0.f : __fdiv_rn(1.0f, __fsqrt_rn(ss));
     if (bad) atomicOr(flags, FLAG_INVALID_INPUT);
@@ -92,14 +116,15 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
                                                      flags);
 }
 
-void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
+void launch_prep_queries(const void* X, bool in_bf16, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
                          float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s, bool pdl,
                          const int32_t* quota, int32_t L, int32_t* quota_dev) {
   const int threads = 256;
   int blocks = (n_pad * 32 + threads - 1) / threads;
   QuotaVec qv{};
   for (int v = 0; v < 32; ++v) qv.v[v] = (quota && v < L) ? quota[v] : 0;
-  launch_pdl_opt(pdl, k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, N, n_pad, d, Xb, inv_q, gthr, ctr, flags,
+  launch_pdl_opt(pdl, k_prep_queries, dim3(blocks), dim3(threads), 0, s, X, (int)in_bf16, N, n_pad, d, Xb, inv_q, gthr,
+                 ctr, flags,
                  qv, quota ? quota_dev : nullptr);
 }
 

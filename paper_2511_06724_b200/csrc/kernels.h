@@ -71,7 +71,8 @@ void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int
 struct QuotaVec {
   int32_t v[32];
 };
-void launch_prep_queries(const float* X, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
+// X is fp32 [N][d], or bf16 [N][d] with in_bf16 (copied as is).
+void launch_prep_queries(const void* X, bool in_bf16, int32_t N, int32_t n_pad, int32_t d, __nv_bfloat16* Xb,
                          float* inv_q, uint64_t* gthr, int32_t* ctr, uint32_t* flags, cudaStream_t s,
                          bool pdl = true, const int32_t* quota = nullptr, int32_t L = 0,
                          int32_t* quota_dev = nullptr);

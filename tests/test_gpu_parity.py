@@ -406,3 +406,46 @@ def test_largest_shapes(argus_mod):
     rep = parity.check_replay(g, opts, quota)
     assert rc == rep["rc"]
     parity.invariants(g, opts, quota)
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_bf16_device_prompts_match_fp32(argus_mod, pipeline):
+    """argus_route_batch_bf16_dev (SURVEY §8(b)'s bf16 device prompts): the fp32 batch
+    rounded to bf16 by torch (RNE, pinned against the oracle's O1) routes bit-identically
+    to the fp32 call; a NaN row fails with ARGUS_E_INVALID at argus_sync."""
+    import torch
+    argus = argus_mod
+    p = gen.small_problem("C1", N=200, M=7000, seed=191)
+    N, k, L = 200, p.k, len(p.opts)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    X = torch.from_numpy(p.X).cuda()
+    Xh = X.to(torch.bfloat16)
+    outs = []
+    with make_router(argus, p, pipeline=pipeline) as r:
+        r.argus_cache_insert(p.cache)
+        for bf in (False, True):
+            o = dict(option=torch.empty(N, dtype=torch.int32, device="cuda"),
+                     topk_idx=torch.empty((N, k), dtype=torch.int32, device="cuda"),
+                     topk_score=torch.empty((N, k), dtype=torch.float32, device="cuda"),
+                     quality=torch.empty((N, L), dtype=torch.float32, device="cuda"),
+                     status=torch.empty(N, dtype=torch.uint8, device="cuda"),
+                     optimal=torch.empty(N, dtype=torch.int32, device="cuda"))
+            fn = r.argus_route_batch_bf16_dev if bf else r.argus_route_batch_ex_dev
+            fn(Xh if bf else X, quota, o["option"], o["topk_idx"], o["topk_score"], o["quality"], o["status"],
+               optimal=o["optimal"])
+            r.argus_sync()
+            outs.append({kk: v.cpu().numpy() for kk, v in o.items()})
+        bad = Xh.clone()
+        bad[5, 3] = float("nan")
+        o = outs[0]
+        r.argus_route_batch_bf16_dev(bad, quota, *(torch.empty_like(torch.from_numpy(v)).cuda() for v in
+                                                   (o["option"], o["topk_idx"], o["topk_score"])))
+        with pytest.raises(argus.ArgusError) as e:
+            r.argus_sync()
+        assert e.value.code == argus.ARGUS_E_INVALID
+    for kk in outs[0]:
+        np.testing.assert_array_equal(outs[0][kk], outs[1][kk], err_msg=kk)
+    g = dict(outs[1])
+    g["topk_idx"] = g["topk_idx"].view(np.uint32)
+    parity.check_topk(p.X, p.cache, k, g["topk_idx"], g["topk_score"], rows=range(0, N, 9))
+    parity.check_replay(g, p.opts, quota)

@@ -3,7 +3,9 @@ times (pipelined router, device-buffer ABI call, batches back to back).
 
 The oracle scans the full cache for a seeded sample of prompts of every batch
 (first, last and random ones: they span every 128-prompt slice's position) and
-replays the predictor (M1) and the assignment (A1, bit-exact) on EVERY prompt.
+replays the predictor (M1) and the assignment (A1, bit-exact) on EVERY prompt.  The
+16-prompt C2 batch also runs the whole oracle route over the 1M-row cache (T3 on every
+prompt, M2, A2 end to end).
 
   C2  M = 1M,  d = 768,  L = 12, bursty sizes 357 / 16 / 512 back to back
   C3  M = 10M, d = 768,  L = 12, N = 256 (one GPU holds all 10M rows: 15.4 GB)
@@ -23,7 +25,7 @@ from tests import parity
 pytestmark = [pytest.mark.gpu, pytest.mark.full]
 
 CASES = {
-    "C2": dict(sizes=[357, 16, 512], sample=16),
+    "C2": dict(sizes=[357, 16, 512], sample=32, e2e_max=16),
     "C3": dict(sizes=[256], sample=16),
     "C4": dict(sizes=[8192], sample=16),
     "C5": dict(sizes=[4096, 4096], sample=16, short_quota_batch=1),
@@ -90,5 +92,10 @@ def test_full_size(name):
         assert err <= parity.SCORE_TOL, err
         rep = parity.check_replay(g, opts, q)                                           # A1 (all prompts)
         parity.invariants(g, opts, q)
+        if n <= case.get("e2e_max", 0):  # small batch: the whole oracle route over the full cache
+            ores = oracle.route(X, cache, k, W1, b1, W2, b2, opts, q, threads=_threads())
+            parity.check_topk(X, cache, k, g["topk_idx"], g["topk_score"])              # T3, every prompt
+            np.testing.assert_allclose(g["quality"], ores["rhat"], atol=parity.SCORE_TOL)  # M2
+            parity.check_e2e(ores, g, opts, q)                                              # A2
         if case.get("short_quota_batch") == b:
             assert rep["rc"] == 1 and int(np.sum(g["status"] & oracle.OVERFLOW)) > 0

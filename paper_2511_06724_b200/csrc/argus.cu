@@ -1161,7 +1161,8 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   } else if (send_seq) {  // K5 + C-2 fused: merged keys stored into every rank's inbox
     {
       StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL, s_scan);
-      launch_merge_send(r->d_partial[q], a.P, N, k, p2p_send_args(r, send_seq), r->d_p2p_ticket, s_scan, !pipelined);
+      launch_merge_send(r->d_partial[q], a.P, N, k, p2p_send_args(r, send_seq), r->d_p2p_ticket, s_scan, !pipelined,
+                        r->num_sms);
     }
     LAUNCHED(r);
   }

@@ -103,9 +103,11 @@ __device__ __forceinline__ uint64_t gtime() {
 template <int KMAX>
 __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t* __restrict__ in, int P, int N, int k,
                                                                 P2PSend dst, int* ticket) {
-  const int i = blockIdx.x;
+  // a capped grid (at most one CTA per SM) loops over the prompts: CTAs spinning on a
+  // credit can never fill the SMs a receiving tail needs to make that credit arrive
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ uint64_t wl[MERGE_WARPS][KMAX];
+  __shared__ uint64_t out_s[KMAX];
   __shared__ int is_last;
   pdl_wait();
   if (threadIdx.x < dst.G && dst.seq > 2) {  // credit: peer's slot of this parity is free again
@@ -119,41 +121,43 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t*
     }
   }
   __syncthreads();
-  TopList<KMAX> l;
-  l.clear();
   const int total = P * k;
   const int per = (total + MERGE_WARPS - 1) / MERGE_WARPS;
   const int e0 = warp * per, e1 = min(total, e0 + per);
   constexpr int B = 8;
-  for (int e = e0 + lane; e < e1; e += 32 * B) {
-    uint64_t buf[B];
+  for (int i = blockIdx.x; i < N; i += gridDim.x) {
+    TopList<KMAX> l;
+    l.clear();
+    for (int e = e0 + lane; e < e1; e += 32 * B) {
+      uint64_t buf[B];
 #pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int ee = e + u * 32;
-      uint64_t key = 0;
-      if (ee < e1) {
-        const int p = ee / k, t = ee - p * k;
-        key = __ldg(reinterpret_cast<const unsigned long long*>(in) + ((int64_t)p * N + i) * k + t);
+      for (int u = 0; u < B; ++u) {
+        const int ee = e + u * 32;
+        uint64_t key = 0;
+        if (ee < e1) {
+          const int p = ee / k, t = ee - p * k;
+          key = __ldg(reinterpret_cast<const unsigned long long*>(in) + ((int64_t)p * N + i) * k + t);
+        }
+        buf[u] = key;
       }
-      buf[u] = key;
-    }
 #pragma unroll
-    for (int u = 0; u < B; ++u) l.insert(buf[u]);
-  }
-  warp_merge_topk<KMAX>(l, k, wl[warp]);
-  __syncthreads();
-  if (warp == 0) {
-    TopList<KMAX> m;
-    m.clear();
-    if (lane < MERGE_WARPS * k) m.insert(wl[lane / k][lane % k]);
-    __shared__ uint64_t out_s[KMAX];
-    warp_merge_topk<KMAX>(m, k, out_s);
-    __syncwarp();
-    // lane (g, t): key t of this prompt into inbox g, slot [rank][i]
-    for (int x = lane; x < dst.G * k; x += 32) {
-      const int g = x / k, t = x - g * k;
-      dst.keys[g][((int64_t)dst.rank * N + i) * k + t] = out_s[t];
+      for (int u = 0; u < B; ++u) l.insert(buf[u]);
     }
+    warp_merge_topk<KMAX>(l, k, wl[warp]);
+    __syncthreads();
+    if (warp == 0) {
+      TopList<KMAX> m;
+      m.clear();
+      if (lane < MERGE_WARPS * k) m.insert(wl[lane / k][lane % k]);
+      warp_merge_topk<KMAX>(m, k, out_s);
+      __syncwarp();
+      // lane (g, t): key t of this prompt into inbox g, slot [rank][i]
+      for (int x = lane; x < dst.G * k; x += 32) {
+        const int g = x / k, t = x - g * k;
+        dst.keys[g][((int64_t)dst.rank * N + i) * k + t] = out_s[t];
+      }
+    }
+    __syncthreads();  // wl / out_s are reused by the next prompt
   }
   __threadfence_system();  // this CTA's peer stores before its ticket
   __syncthreads();
@@ -168,11 +172,12 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t*
 }
 
 void launch_merge_send(const uint64_t* in, int32_t P, int32_t N, int32_t k, const P2PSend& dst, int* ticket,
-                       cudaStream_t s, bool pdl) {
+                       cudaStream_t s, bool pdl, int max_ctas) {
+  const dim3 grid(N < max_ctas ? N : max_ctas);
   if (k <= 4)
-    launch_pdl_opt(pdl, k_merge_send<4>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
+    launch_pdl_opt(pdl, k_merge_send<4>, grid, dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
   else
-    launch_pdl_opt(pdl, k_merge_send<8>, dim3(N), dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
+    launch_pdl_opt(pdl, k_merge_send<8>, grid, dim3(MERGE_WARPS * 32), 0, s, in, P, N, k, dst, ticket);
 }
 
 }  // namespace argus

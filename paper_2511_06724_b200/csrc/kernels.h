@@ -110,8 +110,9 @@ struct P2PSend {
   int32_t G, rank;
   uint32_t seq;
 };
+// grid = min(N, max_ctas) CTAs looping over the prompts (max_ctas = the SM count)
 void launch_merge_send(const uint64_t* in, int32_t P, int32_t N, int32_t k, const P2PSend& dst, int* ticket,
-                       cudaStream_t s, bool pdl);
+                       cudaStream_t s, bool pdl, int max_ctas);
 
 struct TailArgs {
   // phase M: candidate lists -> final top-k

@@ -53,7 +53,7 @@ __global__ void ksd(const uint8_t* rows_g, int n, int L, int Lw, const int* quot
       const int choice = A ? (int)row[__ffs(A) - 1] : 0xFF;
       const bool real = mine && choice != 0xFF;
       uint32_t same, mv;
-      if (MODE == 0) {
+      if (MODE == 0 || MODE == 2) {
         const uint32_t V = __ballot_sync(0xffffffffu, real);
         same = V; mv = V;
 #pragma unroll
@@ -69,11 +69,20 @@ __global__ void ksd(const uint8_t* rows_g, int n, int L, int Lw, const int* quot
         const int src = __ffs(__ballot_sync(0xffffffffu, real && choice == lane)) ;  // not correct in general; timing only
         mv = __shfl_sync(0xffffffffu, same, (src ? src - 1 : 0));
       }
-      const int before = __popc(same & lt);
-      const int remc = __shfl_sync(0xffffffffu, rem_r, choice & 31);
-      const bool ok = !real || before < remc;
-      const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
-      const uint32_t commit = bad ? (pending & ((1u << (__ffs(bad) - 1)) - 1u)) : pending;
+      uint32_t commit;
+      if (MODE == 2) {
+        // lane v: the first lane whose choice v exceeds rem_v (the (rem_v + 1)-th chooser);
+        // the batch commits every pending lane before the earliest such lane
+        const int fe = (lane < 32 && __popc(mv) > rem_r) ? (int)__fns(mv, 0, rem_r + 1) : 32;
+        const int bad_pos = (int)__reduce_min_sync(0xffffffffu, (unsigned)fe);
+        commit = bad_pos >= 32 ? pending : (pending & ((1u << bad_pos) - 1u));
+      } else {
+        const int before = __popc(same & lt);
+        const int remc = __shfl_sync(0xffffffffu, rem_r, choice & 31);
+        const bool ok = !real || before < remc;
+        const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+        commit = bad ? (pending & ((1u << (__ffs(bad) - 1)) - 1u)) : pending;
+      }
       if ((commit >> lane) & 1u) opt_s[jj] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
       rem_r -= __popc(mv & commit);
       avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
@@ -107,8 +116,12 @@ int main() {
   for (int rep = 0; rep < 3; ++rep) {
     ksd<0><<<1, 32>>>(drows, n, L, Lw, dq, o, dopt); cudaMemcpy(r, o, 16, cudaMemcpyDeviceToHost);
     printf("ballots: %llu cycles, %llu steps, %.0f cycles/step\n", r[0], r[1], (double)r[0] / r[1]);
-    ksd<1><<<1, 32>>>(drows, n, L, Lw, dq, o, dopt); cudaMemcpy(r, o, 16, cudaMemcpyDeviceToHost);
-    printf("match  : %llu cycles, %llu steps, %.0f cycles/step\n", r[0], r[1], (double)r[0] / r[1]);
+    int opt0[64], opt2[64];
+    cudaMemcpy(opt0, dopt, 64 * 4, cudaMemcpyDeviceToHost);
+    ksd<2><<<1, 32>>>(drows, n, L, Lw, dq, o, dopt); cudaMemcpy(r, o, 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(opt2, dopt, 64 * 4, cudaMemcpyDeviceToHost);
+    int same = 1; for (int i = 0; i < n; ++i) same &= opt0[i] == opt2[i];
+    printf("fns+min: %llu cycles, %llu steps, %.0f cycles/step, same assignment %d\n", r[0], r[1], (double)r[0] / r[1], same);
   }
   return 0;
 }

@@ -16,6 +16,12 @@ import oracle
 
 SCORE_TOL = 2e-2    # T1, M1, M2
 GAP_TOL = 1e-3      # T3 boundary-gap exemption, A2 fragility
+# Bounds on the loosely checked share (SURVEY §8(c).iii "report the exemption rate"):
+# clustered caches put several rows within 1e-3 of a prompt's k-th score, so T3 leaves
+# 30-80 % of rows to its tie-group rule at these sizes (T2 checks them exactly); a rate
+# above this bound means the synthetic workload degenerated (e.g. all-duplicate rows)
+# and the top-k parity would be checking little.
+MAX_T3_EXEMPT_RATE = 0.9
 DELTA32 = float(np.float32(oracle.DELTA))
 
 # Per-test parity statistics (T3 exemption rates, A2 matched-prefix fractions, T2
@@ -98,6 +104,8 @@ def check_topk(X, cache, k, gpu_idx, gpu_score, ids=None, rows=None):
     nrows = len(list(rows))
     report("T3", rows=nrows, exempt_rows=exempt, exempt_rate=round(exempt / max(1, nrows), 4), M=int(M), k=int(k),
            max_score_err=max_err)
+    if nrows >= 20:
+        assert exempt / nrows <= MAX_T3_EXEMPT_RATE, (exempt, nrows)
     return dict(exempt_rows=exempt, max_score_err=max_err, rows=nrows)
 
 

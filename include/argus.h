@@ -112,13 +112,18 @@ typedef struct {
  *   evict      0: an insert past capacity fails (ARGUS_E_CAPACITY).  1: ring
  *              eviction of the oldest entries (capacity % world == 0); see
  *              argus_cache_insert_h
- *   pipeline   0: every call's work is ordered on `stream`.  1 (single GPU,
- *              argus_route_batch_dev only): the fused tail of batch b (merge,
+ *   pipeline   0: every call's work is ordered on `stream`.  1 (device and
+ *              asynchronous host calls): the fused tail of batch b (merge,
  *              predictor, A5, assignment) runs on an internal high-priority
  *              stream and overlaps the scan of batch b+1; the outputs of a call
  *              are complete once argus_route_join / argus_sync says so.  The
  *              prompt buffer of a call may be reused as soon as `stream` has
- *              passed the call (the prompts are consumed by the scan part). */
+ *              passed the call (the prompts are consumed by the scan part).
+ *              With NCCL the collectives run on one internal stream in program
+ *              order and batch b's exchange + tail are issued by call b+1 (or by
+ *              argus_route_join / argus_sync / argus_route_wait); on the
+ *              ncclAllGather fallback path those draining calls issue a collective,
+ *              so every rank must make them at the same point of its call sequence. */
 typedef struct {
   int32_t d, k, L, hidden;
   int32_t max_batch;

@@ -206,3 +206,25 @@ def test_g_invariance_migrating_pairs(argus_mod):
     parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"], rows=rows)
     parity.check_replay(g, p.opts, quota)
     parity.invariants(g, p.opts, quota)
+
+
+@pytest.mark.parametrize("L,H,d,k,N,M", [(1, 32, 64, 1, 1, 1), (2, 32, 64, 2, 5, 3), (1, 64, 128, 4, 40, 700),
+                                         (3, 96, 192, 3, 17, 1500)])
+def test_smallest_shapes(argus_mod, L, H, d, k, N, M):
+    """The ABI's smallest shapes: one or two options, the narrowest predictor (H = 32),
+    d = 64, k = 1, a single prompt, a single cached row; T2 exact, M1, A1 bit-exact."""
+    argus = argus_mod
+    p = gen.small_problem("C1", N=N, M=M, d=d, k=k, seed=271 + L + H)
+    opts = gen.option_table(("SD-XL", "Tiny-SD"), (0, 10, 20))[:L]
+    W1, b1, W2, b2 = gen.mlp_weights(d, k, H, L)
+    quota = np.full(L, N // L + 1, np.int32)
+    with argus.Router(d, k, opts, W1, b1, W2, b2, capacity=M + 8, max_batch=N) as r:
+        r.argus_cache_insert(p.cache)
+        rc, g, S = route_captured(argus, r, p.X, quota, M)
+    parity.check_topk_replay(S, g["topk_idx"], g["topk_score"], k)
+    parity.check_topk(p.X, p.cache, k, g["topk_idx"], g["topk_score"])
+    err = float(np.abs(oracle.mlp(p.X, g["topk_score"].astype(np.float64), W1, b1, W2, b2) - g["quality"]).max())
+    assert err <= parity.SCORE_TOL
+    rep = parity.check_replay(g, opts, quota)
+    assert rc == rep["rc"]
+    parity.invariants(g, opts, quota)

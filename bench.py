@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--sweep", default="", help="comma list of fixed N: per-N stage times to stderr")
     ap.add_argument("--fixed-n", type=int, default=0, help="diagnostics: every batch has this N")
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="diagnostics: one GPU's stripe of a G-GPU run (M / G rows), to bound per-GPU throughput "
+                         "at G GPUs without the cross-GPU collectives")
     ap.add_argument("--force-nccl", action="store_true",
                     help="diagnostics: on one GPU, run the multi-GPU data path through a one-rank NCCL communicator")
     ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
@@ -243,6 +246,10 @@ def main():
     args = parse()
     rank, world, local_rank = dist_env()
     cfg = gen.CONFIGS[args.config]
+    if args.shard_of > 1:  # diagnostics: what one GPU of a G-GPU run scans
+        import dataclasses
+        cfg = dataclasses.replace(cfg, M=cfg.M // args.shard_of,
+                                  note=f"{cfg.note} [one GPU's stripe of {args.shard_of}: M / {args.shard_of}]")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args)
     if args.gpus != world:

@@ -1136,7 +1136,10 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
         a.floaters = 0;
       }
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;  // cannot happen (see init)
-      if (launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, !pipelined) != cudaSuccess) {
+      // PDL also when pipelined: consecutive kernels of the scan stream (scan, merge, next
+      // scan) overlap prologue and drain; the buffers of the next batch are another parity
+      // and its cross-stream inputs are ordered by events
+      if (launch_scan_pair(a, &r->tmap_c32, &r->tmap_q[q], s_scan, true) != cudaSuccess) {
         // cluster launch refused (configuration, not a device fault): one slice per CTA from now on
         cudaGetLastError();
         r->pair_scan = false;
@@ -1147,7 +1150,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
     if (!pair) {
       a.P = scan_plan_ranges(a.m_local, N, scan_sms);
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;
-      launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, !pipelined);
+      launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, true);
     }
   }
   LAUNCHED(r);
@@ -1161,7 +1164,7 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   } else if (send_seq) {  // K5 + C-2 fused: merged keys stored into every rank's inbox
     {
       StageScope sc(r, ARGUS_STAGE_MERGE_LOCAL, s_scan);
-      launch_merge_send(r->d_partial[q], a.P, N, k, p2p_send_args(r, send_seq), r->d_p2p_ticket, s_scan, !pipelined,
+      launch_merge_send(r->d_partial[q], a.P, N, k, p2p_send_args(r, send_seq), r->d_p2p_ticket, s_scan, true,
                         r->num_sms);
     }
     LAUNCHED(r);

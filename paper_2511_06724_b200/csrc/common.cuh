@@ -68,6 +68,16 @@ struct TopList {
     for (int i = 0; i < KMAX; ++i) v[i] = 0;
   }
   __device__ __forceinline__ uint64_t min_key() const { return v[KMAX - 1]; }
+  // branch-free insert: KMAX compare-exchanges whatever the key (for loops over many
+  // keys: a data-dependent early exit there costs more than the network)
+  __device__ __forceinline__ void insert_nb(uint64_t y) {
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      const uint64_t hi = v[i] > y ? v[i] : y, lo = v[i] > y ? y : v[i];
+      v[i] = hi;
+      y = lo;
+    }
+  }
   __device__ __forceinline__ void insert(uint64_t key) {
     if (key <= v[KMAX - 1]) return;
     v[KMAX - 1] = key;

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_topk(const uint64_t*
       buf[u] = key;
     }
 #pragma unroll
-    for (int u = 0; u < B; ++u) l.insert(buf[u]);
+    for (int u = 0; u < B; ++u) l.insert_nb(buf[u]);
   }
   warp_merge_topk<KMAX>(l, k, wl[warp]);
   __syncthreads();
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t*
         buf[u] = key;
       }
 #pragma unroll
-      for (int u = 0; u < B; ++u) l.insert(buf[u]);
+      for (int u = 0; u < B; ++u) l.insert_nb(buf[u]);
     }
     warp_merge_topk<KMAX>(l, k, wl[warp]);
     __syncthreads();

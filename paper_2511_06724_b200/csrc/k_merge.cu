@@ -159,13 +159,19 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) k_merge_send(const uint64_t*
     }
     __syncthreads();  // wl / out_s are reused by the next prompt
   }
-  __threadfence_system();  // this CTA's peer stores before its ticket
+  // The CTA's peer stores are released by its ticket increment (acq_rel, system scope,
+  // after the CTA barrier, which makes every thread's stores part of thread 0's release);
+  // the last CTA's increment acquires all of them and its release store of each flag
+  // publishes them (cumulativity) -- no sequentially consistent system fence needed.
   __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    is_last = old == gridDim.x - 1;
+  }
   __syncthreads();
   pdl_launch();
   if (is_last && threadIdx.x < dst.G) {
-    __threadfence_system();
     st_release_sys(dst.flag[threadIdx.x], dst.seq);
     if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
   }

@@ -75,6 +75,22 @@ def test_t2_exact_topk_replay(argus_mod, N, M, k, seed):
     assert rc == rep["rc"]
 
 
+@pytest.mark.parametrize("N,M,d,seed", [(64, 4096, 1024, 281), (256, 9000, 1024, 282), (300, 6000, 1024, 283),
+                                        (100, 5000, 832, 284), (200, 7000, 64, 285)])
+def test_t2_exact_wide_embeddings(argus_mod, N, M, d, seed):
+    """T2 on the d > 768 variants (k-blocks 12.. of the prompt slice read from shared
+    memory, quarter-tile slots) of both scans, and on a narrow d = 64."""
+    p = gen.small_problem("C1", N=N, M=M, d=d, seed=seed)
+    quota = oracle.quota_from_fractions(p.fractions, N)
+    with make_router(argus_mod, p) as r:
+        r.argus_cache_insert(p.cache)
+        rc, g, S = route_captured(argus_mod, r, p.X, quota, M)
+    parity.check_topk_replay(S, g["topk_idx"], g["topk_score"], p.k)
+    parity.check_topk(p.X, p.cache, p.k, g["topk_idx"], g["topk_score"], rows=list(range(0, N, 5)))
+    rep = parity.check_replay(g, p.opts, quota)
+    assert rc == rep["rc"]
+
+
 @pytest.mark.parametrize("G", [2, 3])
 def test_t2_striped_shards(argus_mod, G):
     """Each shard's captured scores, placed at global ids g = slot * G + rank, re-ranked

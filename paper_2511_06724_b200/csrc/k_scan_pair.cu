@@ -578,13 +578,18 @@ cudaError_t launch_scan_pair(const ScanArgs& a, const CUtensorMap* tmap_c32, con
   const int pslices = (a.N + 2 * TM - 1) / (2 * TM);
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   const dim3 grid(a.migrate ? a.grid_ctas : 2 * pslices * a.P);
-  // several 128-prompt slices re-read each tile: normal L2 policy (ARGUS_SCAN_L2 overrides)
+  // L2 policy of the cache stream: evict-first at every slice count.  Even when
+  // several pair slices re-read a tile, evict-first is the lower-DRAM choice:
+  // the slices run a few tiles apart, so a tile is re-read while it is still the
+  // newest line in its set, and marking it evict-first keeps the older ring
+  // traffic from pushing it out (C4 N = 8192: 9.71 GB normal, 8.24 GB evict-first
+  // against 8.21 GB algorithmic; profiles/r02/l2_policy.md).  ARGUS_SCAN_L2 overrides.
   static int l2env = -2;
   if (l2env == -2) {
     const char* e = getenv("ARGUS_SCAN_L2");
     l2env = e ? atoi(e) : -1;
   }
-  const int l2mode = l2env >= 0 ? l2env : (pslices == 1 ? 0 : 1);
+  const int l2mode = l2env >= 0 ? l2env : 0;
   const bool wide = a.d / KBLK > KB_TMEM;
   const bool clip = a.d == KB_TMEM * KBLK;  // d = 768 (CLIP): compile-time k-block count
   const bool clip_h = a.d == KB_MAX * KBLK;  // d = 1024 (OpenCLIP-H)

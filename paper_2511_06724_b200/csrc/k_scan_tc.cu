@@ -407,15 +407,16 @@ void launch_scan(const ScanArgs& a, const CUtensorMap* tmap, const CUtensorMap* 
   const int slices = (a.N + TM - 1) / TM;
   const int64_t n_tiles = (a.m_local + TN - 1) / TN;
   const dim3 grid(slices * a.P);
-  // L2 policy of the cache stream: evict-first for one slice, normal LRU when
-  // several slices re-read each tile (ARGUS_SCAN_L2=0/1/2 overrides, experiments)
+  // L2 policy of the cache stream: evict-first (measured no worse than normal LRU
+  // with several slices either, profiles/r02/l2_policy.md; ARGUS_SCAN_L2=1/2
+  // overrides for multi-slice experiments)
   static int l2env = -2;
   if (l2env == -2) {
     const char* e = getenv("ARGUS_SCAN_L2");
     l2env = e ? atoi(e) : -1;
   }
   static int stat = getenv("ARGUS_SCAN_1MMA") ? 32 : 0;
-  const int l2mode = (l2env >= 0 ? (slices == 1 ? 0 : l2env) : (slices == 1 ? 0 : 1)) | stat;
+  const int l2mode = (l2env >= 0 && slices > 1 ? l2env : 0) | stat;
   const bool wide = a.d / KBLK > KB_TMEM;
   const bool clip = a.d == KB_TMEM * KBLK, clip_h = a.d == KB_MAX * KBLK;  // d = 768 / 1024
   if (a.k <= 4) {

@@ -126,7 +126,7 @@ struct argus_router {
   float* d_score = nullptr;        // [max_batch][k]
   uint32_t* d_idx = nullptr;       // [max_batch][k]
   float* d_rhat = nullptr;         // [max_batch][L]
-  uint8_t* d_pref = nullptr;       // [max_batch][L] pi_i as a list of options
+  uint8_t* d_pref = nullptr;       // [max_batch][32] pi_i in inverse form (rank of each option)
   uint8_t* d_ccount = nullptr;     // [max_batch]
   uint32_t* d_cmask = nullptr;     // [max_batch]
   uint8_t* d_status = nullptr;     // [max_batch]
@@ -726,7 +726,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   TRY_RC(dalloc(r, &r->d_score, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_idx, (size_t)c.max_batch * k));
   TRY_RC(dalloc(r, &r->d_rhat, (size_t)c.max_batch * L));
-  TRY_RC(dalloc(r, &r->d_pref, (size_t)c.max_batch * ((L + 3) / 4 * 4)));
+  TRY_RC(dalloc(r, &r->d_pref, (size_t)c.max_batch * 32));
   TRY_RC(dalloc(r, &r->d_ccount, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_cmask, (size_t)c.max_batch));
   TRY_RC(dalloc(r, &r->d_status, (size_t)c.max_batch));
@@ -1247,9 +1247,12 @@ static int finish_impl(argus_router* r, const uint64_t* keys_in, int32_t P, int3
   m.k = k;
   m.H = r->cfg.hidden;
   m.L = L;
-  m.Lw = (L + 3) / 4 * 4;
   m.rhat = quality_dev ? quality_dev : r->d_rhat;
   m.prefl = r->d_pref;
+  {  // serial dictatorship schedule: one prompt per step up to sd_pp_max prompts (k_tail.cu)
+    static const int pp_env = getenv("ARGUS_SD_PP") ? atoi(getenv("ARGUS_SD_PP")) : -1;
+    m.sd_pp_max = pp_env >= 0 ? pp_env : 512;  // measured in situ: per-prompt <= windows up to N = 512
+  }
   m.ccount = r->d_ccount;
   m.cmask = r->d_cmask;
   // quotas travel by value in the kernel parameter block (no host buffer lifetime issue)

@@ -19,12 +19,13 @@
 // Layer 1 runs on mma.sync m16n8k16 (bf16, fp32 accumulate): the whole predictor is
 // < 0.03 % of the scan's flops and this product (16 x d x 32 per CTA) is far below a
 // tcgen05 tile.  W1x is pre-arranged at init in per-lane fragment order so each B
-// fragment is one coalesced 8-byte load.  In phase 2 one warp owns one prompt and
+// fragment is one coalesced 8-byte load.  In phase 2 one warp owns two prompts and
 // lane v owns option v (L <= 32): masks are ballots, the preference rank is a
-// 32-lane compare-count, scattered into the list pi_i that phase 3 consumes.  Phase 3
-// runs the serial dictatorship 32 prompts at a time in one warp: each lane takes the
-// first option of its pi_i with quota left, and the group commits up to the first
-// lane whose option the earlier lanes used up (at most N/32 + L group steps).
+// branch-free compare-count against the static (p_th, index) order, o_i three warp
+// reductions, and pi_i goes to phase 3 in inverse form (rank of each option, one
+// 32-byte row per prompt).  Phase 3 runs the serial dictatorship in one warp, one
+// prompt per redux.sync step (lane = option) or, for large batches, 32 prompts per
+// window step (lane = prompt; see assign_all).
 #include <cstdio>
 
 #include "common.cuh"
@@ -106,46 +107,63 @@ static size_t phase1_bytes(int d, int k, int P_max) {
 static size_t phase2_bytes(int d, int H, int L) {
   return w2_offset(d, H) + sizeof(float) * ((size_t)L * (H + 4) + (size_t)TW * (PB / TW) * 32 + 32);  // W2 | r | p_th
 }
-// Phase 3 layout: [order: N i32][cc: N u8, padded to 16][rk: CH x Lw u8][cm: CH u32][st: CH u8][opt: CH u8]
-// [inv: 32 x 32 u8, the SD warp's per-lane inverse of pi].
-// With N <= CH ("by index") rk / cm / st hold every prompt's row at its index, staged in the
-// same round trip as |C_i|; larger batches stage rows chunk by chunk in priority order.
-__host__ __device__ __forceinline__ size_t p3_rk_offset(int N) {
-  return sizeof(int32_t) * (size_t)N + (((size_t)N + 15) & ~(size_t)15);
+// Phase 3 layout: [order: N i32][cc: N u8, padded to 16][rk: CH x 32 u8][cm: CH u32][st: CH u8]
+// [opt: CH u8][lst: 32 x 32 u8, the window warp's per-lane pi as a list].
+// rk rows are pi_i in inverse form (rank of option v in pi_i, 0xFF if v is not admissible),
+// as phase 2 writes them.  With N <= CH ("by index") rk / cm / st hold every prompt's row
+// at its index, staged in the same round trip as |C_i|; larger batches stage rows chunk by
+// chunk in priority order.
+__host__ __device__ __forceinline__ size_t p3_rk_offset(int N) {  // 16-byte aligned
+  return ((sizeof(int32_t) * (size_t)N + 15) & ~(size_t)15) + (((size_t)N + 15) & ~(size_t)15);
 }
-static size_t phase3_bytes(int N, int L) {
-  const int Lw = (L + 3) / 4 * 4;
-  return p3_rk_offset(N) + (size_t)CH * Lw + sizeof(uint32_t) * CH + 2 * (size_t)CH + 32 * 32;
+static size_t phase3_bytes(int N) {
+  return p3_rk_offset(N) + (size_t)CH * 32 + sizeof(uint32_t) * CH + 2 * (size_t)CH + 32 * 32;
 }
 
 size_t tail_smem_bytes(int d, int k, int H, int L, int max_batch, int P_max) {
   size_t b = phase1_bytes(d, k, P_max);
   b = b > phase2_bytes(d, H, L) ? b : phase2_bytes(d, H, L);
-  b = b > phase3_bytes(max_batch, L) ? b : phase3_bytes(max_batch, L);
+  b = b > phase3_bytes(max_batch) ? b : phase3_bytes(max_batch);
   return b;
 }
 
 // ------------------------------------------------------------------ phase 3
+// Serial dictatorship: prompts in priority order, each takes the first option of
+// its pi_i whose quota is not used up.  Two exact schedules of the same sequential result:
+//  * one prompt per step (small batches): lane v = option v offers its rank in pi_i while
+//    rem_v > 0; the prompt's choice is the lane of the minimum offer (one redux.sync), and
+//    that lane decrements rem_v -- select, redux, compare, decrement per prompt (67 cycles
+//    on one warp, tools/sd_bench.cu);
+//  * windows of 32 prompts (large batches), lane = prompt: every pending lane takes the
+//    first option of its pi with quota left; the choices equal the sequential ones up to the
+//    first lane whose option earlier pending lanes used up (their count >= rem), so those
+//    lanes commit and the rest retry.  An option runs out at most once, so a window takes at
+//    most 1 + L steps (about 615 cycles each).
+// On one warp (tools/sd_bench.cu) the per-prompt schedule takes 67 N cycles and the windows
+// about 615 (N / 32 + L); inside the tail (cold code, the timing build's phase stamps) 85-90
+// cycles per prompt against 1300 per window step, so prompts go one per step up to
+// TailArgs::sd_pp_max = 512 (equal times there), windows beyond.
 __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
-  const int N = a.N, L = a.L, Lw = a.Lw;
+  const int N = a.N, L = a.L;
   const bool byidx = N <= CH;
+  const bool small = N <= TT;  // priority order by a compare-count instead of the counting sort
+  const bool pp = byidx && N <= a.sd_pp_max;
   int32_t* order_s = reinterpret_cast<int32_t*>(smraw);                   // [N]
   uint8_t* cc_s = smraw + sizeof(int32_t) * (size_t)N;                    // [N]
-  uint8_t* rk_s = smraw + p3_rk_offset(N);                                 // [CH][Lw]
-  uint32_t* cm_s = reinterpret_cast<uint32_t*>(rk_s + (size_t)CH * Lw);   // [CH]
+  uint8_t* rk_s = smraw + p3_rk_offset(N);                                 // [CH][32]
+  uint32_t* cm_s = reinterpret_cast<uint32_t*>(rk_s + (size_t)CH * 32);   // [CH]
   uint8_t* st_s = reinterpret_cast<uint8_t*>(cm_s + CH);                   // [CH]
   uint8_t* opt_s = st_s + CH;                                              // [CH] (option | 0x80 overflow)
   __shared__ int32_t base[NB];
   __shared__ int32_t tot[NB];
   __shared__ int32_t wcnt[TW][NB];
   __shared__ int32_t rem_s[32];
+  __shared__ __align__(16) uint16_t key_s[TT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t* rk32 = reinterpret_cast<const uint32_t*>(a.prefl);
-  const int W = Lw / 4;
+  const uint4* rk16 = reinterpret_cast<const uint4*>(a.prefl);
   TS(12);
 
-  // one round trip: |C_i| of every prompt (and, by index, its mask, pi_i and status),
-  // then a warp-aggregated histogram of |C_i|
+  // one round trip: |C_i| of every prompt (and, by index, its mask, pi_i and status)
   if (tid < NB) base[tid] = 0;
   if (tid < 32) {
     int c = tid < L ? (a.quota_dev ? a.quota_dev[tid] : a.quota[tid]) : 0;
@@ -155,185 +173,250 @@ __device__ void assign_all(const TailArgs& a, uint8_t* smraw) {
     }
     rem_s[tid] = c;
   }
-  __syncthreads();
-  for (int i0 = 0; i0 < N; i0 += TT) {
-    const int i = i0 + tid;
-    const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
-    if (byidx && i < N) {
+  if (small) {
+    // priority position of prompt i = #{j : (|C_j|, j) < (|C_i|, i)}: 16-bit keys |C| << 10 | i
+    const int i = tid;
+    uint32_t key = 0xFFFFu;
+    if (i < N) {
+      const int b = (int)__ldcg(a.ccount + i);
       cm_s[i] = __ldcg(a.cmask + i);
       st_s[i] = __ldcg(a.status + i);
-      uint32_t wd[8];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) wd[w] = w < W ? __ldcg(rk32 + (int64_t)i * W + w) : 0u;
-#pragma unroll
-      for (int w = 0; w < 8; ++w)
-        if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)i * Lw)[w] = wd[w];
+      const uint4 w0 = __ldcg(rk16 + 2 * i), w1 = __ldcg(rk16 + 2 * i + 1);
+      reinterpret_cast<uint4*>(rk_s)[2 * i] = w0;
+      reinterpret_cast<uint4*>(rk_s)[2 * i + 1] = w1;
+      key = (uint32_t)b << 10 | (uint32_t)i;
     }
-    if (i < N) cc_s[i] = (uint8_t)b;
-    const uint32_t peers = __match_any_sync(0xffffffffu, b);
-    if (b >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&base[b], __popc(peers));
-  }
-  __syncthreads();
-  TS(13);
-  if (warp == 0) {  // exclusive scan of the 33 bucket counts
-    const int c0 = base[lane];
-    int x = c0;
-#pragma unroll
-    for (int m = 1; m < 32; m <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, m);
-      if (lane >= m) x += y;
-    }
-    const int tot31 = __shfl_sync(0xffffffffu, x, 31);
-    base[lane] = x - c0;
-    if (lane == 0) base[32] = tot31;
-  }
-  __syncthreads();
-  for (int c0 = 0; c0 < N; c0 += TT) {  // stable scatter into priority order
-    const int i = c0 + tid;
-    const int b = i < N ? (int)cc_s[i] : -1;
-    for (int x = tid; x < TW * NB; x += TT) (&wcnt[0][0])[x] = 0;
+    key_s[tid] = (uint16_t)key;
     __syncthreads();
-    const uint32_t peers = __match_any_sync(0xffffffffu, b);
-    const int wrank = __popc(peers & ((1u << lane) - 1u));
-    if (b >= 0 && wrank == 0) wcnt[warp][b] = __popc(peers);
-    __syncthreads();
-    if (tid < NB) {
-      int run = 0;
+    TS(13);
+    if (i < N) {
+      int pos = 0;
+      const uint4* k4 = reinterpret_cast<const uint4*>(key_s);
+#pragma unroll 2
+      for (int j8 = 0; j8 < (N + 7) / 8; ++j8) {  // 8 keys per 16-byte broadcast read
+        const uint4 w = k4[j8];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int w = 0; w < TW; ++w) { const int c = wcnt[w][tid]; wcnt[w][tid] = run; run += c; }
-      tot[tid] = run;
+        for (int h = 0; h < 4; ++h) pos += (int)((ws[h] & 0xFFFFu) < key) + (int)((ws[h] >> 16) < key);
+      }
+      order_s[pos] = i;
     }
     __syncthreads();
-    if (b >= 0) order_s[base[b] + wcnt[warp][b] + wrank] = i;
+  } else {
+    // counting sort by |C_i| (stable): warp-aggregated histogram, scan, ordered scatter
     __syncthreads();
-    if (tid < NB) base[tid] += tot[tid];
+    for (int i0 = 0; i0 < N; i0 += TT) {
+      const int i = i0 + tid;
+      const int b = i < N ? (int)__ldcg(a.ccount + i) : -1;
+      if (byidx && i < N) {
+        cm_s[i] = __ldcg(a.cmask + i);
+        st_s[i] = __ldcg(a.status + i);
+        const uint4 w0 = __ldcg(rk16 + 2 * i), w1 = __ldcg(rk16 + 2 * i + 1);
+        reinterpret_cast<uint4*>(rk_s)[2 * i] = w0;
+        reinterpret_cast<uint4*>(rk_s)[2 * i + 1] = w1;
+      }
+      if (i < N) cc_s[i] = (uint8_t)b;
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      if (b >= 0 && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&base[b], __popc(peers));
+    }
+    __syncthreads();
+    TS(13);
+    if (warp == 0) {  // exclusive scan of the 33 bucket counts
+      const int c0 = base[lane];
+      int x = c0;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, m);
+        if (lane >= m) x += y;
+      }
+      const int tot31 = __shfl_sync(0xffffffffu, x, 31);
+      base[lane] = x - c0;
+      if (lane == 0) base[32] = tot31;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < N; c0 += TT) {  // stable scatter into priority order
+      const int i = c0 + tid;
+      const int b = i < N ? (int)cc_s[i] : -1;
+      for (int x = tid; x < TW * NB; x += TT) (&wcnt[0][0])[x] = 0;
+      __syncthreads();
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      const int wrank = __popc(peers & ((1u << lane) - 1u));
+      if (b >= 0 && wrank == 0) wcnt[warp][b] = __popc(peers);
+      __syncthreads();
+      if (tid < NB) {
+        int run = 0;
+#pragma unroll
+        for (int w = 0; w < TW; ++w) { const int c = wcnt[w][tid]; wcnt[w][tid] = run; run += c; }
+        tot[tid] = run;
+      }
+      __syncthreads();
+      if (b >= 0) order_s[base[b] + wcnt[warp][b] + wrank] = i;
+      __syncthreads();
+      if (tid < NB) base[tid] += tot[tid];
+    }
+    __syncthreads();
   }
-  __syncthreads();
 
-  // serial dictatorship over chunks of the priority order
   TS(14);
   bool any_overflow = false;
-  int rem_r = rem_s[lane];                                          // warp 0: lane v holds rem_v
+  int rem_r = rem_s[lane];  // warp 0: lane v holds rem_v
   if (ARGUS_TAIL_TIMING && tid == 0) tail_ts[22] = 0;
-  uint32_t avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
-  for (int c0 = 0; c0 < N; c0 += CH) {
-    const int n = min(CH, N - c0);
-    if (!byidx) {
-      for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
-        int ii[4];
+  if (pp) {
+    if (warp == 0) {
+      // the rows of the next 4 prompts are read while the current 4 are decided, so the
+      // chain per prompt is only select -> redux -> compare -> decrement
+      auto rows4 = [&](int t0, uint32_t (&rk)[4]) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rk[u] = t0 + u < N ? rk_s[(size_t)order_s[t0 + u] * 32 + lane] : 0xFFu;
+      };
+      uint32_t cur[4], nxt[4];
+      rows4(0, cur);
+#pragma unroll 1
+      for (int t0 = 0; t0 < N; t0 += 4) {
+        rows4(t0 + 4, nxt);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int t = t0 + u * TT;
-          ii[u] = t < n ? order_s[c0 + t] : -1;
+          const uint32_t mine = cur[u] << 5 | (uint32_t)lane;
+          const uint32_t offer = (rem_r > 0 && cur[u] != 0xFFu) ? mine : 0xFFFFu;
+          const uint32_t m = __reduce_min_sync(0xffffffffu, offer);
+          rem_r -= (m == mine) ? 1 : 0;  // only the chosen lane's offer equals m
+          const bool live = t0 + u < N;
+          if (lane == 0 && live) opt_s[t0 + u] = m == 0xFFFFu ? (uint8_t)0x80 : (uint8_t)(m & 31u);
+          any_overflow |= live && m == 0xFFFFu;
         }
-        uint32_t cm[4];
-        uint8_t st[4];
-        uint32_t wd[4][8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          cm[u] = ii[u] >= 0 ? __ldcg(a.cmask + ii[u]) : 0u;
-          st[u] = ii[u] >= 0 ? __ldcg(a.status + ii[u]) : (uint8_t)0;
+        for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+      }
+      if (ARGUS_TAIL_TIMING && lane == 0) tail_ts[22] = N;
+    }
+    __syncthreads();
+    TS(15);
+    for (int t = tid; t < N; t += TT) {
+      const int i = order_s[t];
+      const int o = opt_s[t] & 0x7F;
+      uint8_t st = st_s[i];
+      if (opt_s[t] & 0x80) st |= 1u;              // ARGUS_ST_OVERFLOW (option 0)
+      if (!((cm_s[i] >> o) & 1u)) st |= 2u;       // ARGUS_ST_NONCOMPLIANT
+      a.status[i] = st;
+      a.option_out[i] = o;
+    }
+  } else {
+    uint32_t avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
+    for (int c0 = 0; c0 < N; c0 += CH) {
+      const int n = min(CH, N - c0);
+      if (!byidx) {
+        for (int t0 = tid; t0 < n; t0 += 4 * TT) {  // gather rows in priority order, 4 rows in flight
+          int ii[4];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) wd[u][w] = (ii[u] >= 0 && w < W) ? __ldcg(rk32 + (int64_t)ii[u] * W + w) : 0u;
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * TT;
+            ii[u] = t < n ? order_s[c0 + t] : -1;
+          }
+          uint32_t cm[4];
+          uint8_t st[4];
+          uint4 wd[4][2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cm[u] = ii[u] >= 0 ? __ldcg(a.cmask + ii[u]) : 0u;
+            st[u] = ii[u] >= 0 ? __ldcg(a.status + ii[u]) : (uint8_t)0;
+            wd[u][0] = ii[u] >= 0 ? __ldcg(rk16 + 2 * ii[u]) : make_uint4(0, 0, 0, 0);
+            wd[u][1] = ii[u] >= 0 ? __ldcg(rk16 + 2 * ii[u] + 1) : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * TT;
+            if (t < n) {
+              cm_s[t] = cm[u];
+              st_s[t] = st[u];
+              reinterpret_cast<uint4*>(rk_s)[2 * t] = wd[u][0];
+              reinterpret_cast<uint4*>(rk_s)[2 * t + 1] = wd[u][1];
+            }
+          }
         }
+        __syncthreads();
+      }
+      if (warp == 0) {
+        // lane = rank in the window; each lane keeps the ranks (positions in its pi) still
+        // available as a bit mask A, clears the rank of each option that ran out (its row of
+        // rk_s is the inverse of pi) and reads its choice at the lowest remaining rank from
+        // its pi as a list (lst, built from the inverse row)
+        uint8_t* lst = opt_s + CH + lane * 32;
+#pragma unroll 1
+        for (int t0 = 0; t0 < n; t0 += 32) {
+          const int jj = t0 + lane;
+          const bool act = jj < n;
+          const uint8_t* inv = rk_s + (size_t)(act ? (byidx ? order_s[c0 + jj] : jj) : 0) * 32;
+          uint32_t A = 0;  // ranks whose option has quota left
+          if (act) {  // branch-free: predicated stores, masks by select
+            const uint32_t* inv32 = reinterpret_cast<const uint32_t*>(inv);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int t = t0 + u * TT;
-          if (t < n) {
-            cm_s[t] = cm[u];
-            st_s[t] = st[u];
+            for (int q = 0; q < 8; ++q) {
+              if (4 * q < L) {  // uniform
+                const uint32_t w = inv32[q];
 #pragma unroll
-            for (int w = 0; w < 8; ++w)
-              if (w < W) reinterpret_cast<uint32_t*>(rk_s + (size_t)t * Lw)[w] = wd[u][w];
+                for (int b = 0; b < 4; ++b) {
+                  const int v = 4 * q + b;
+                  const uint32_t r = (w >> (8 * b)) & 0xFFu;  // 0xFF for v >= L too
+                  const bool ok = r != 0xFFu;
+                  if (ok) lst[r] = (uint8_t)v;
+                  A |= (ok && ((avail_r >> v) & 1u)) ? (1u << (r & 31u)) : 0u;
+                }
+              }
+            }
+          }
+          __syncwarp();
+          uint32_t pending = __ballot_sync(0xffffffffu, act);
+          const uint32_t lt = (1u << lane) - 1u;
+          uint32_t seen = avail_r;  // options whose exhaustion A already reflects
+#pragma unroll 1
+          while (pending) {
+            for (uint32_t ex = seen & ~avail_r; ex; ex &= ex - 1) {  // options that ran out
+              const uint32_t r = inv[__ffs(ex) - 1];
+              if (r != 0xFFu) A &= ~(1u << r);
+            }
+            seen = avail_r;
+            const bool mine = (pending >> lane) & 1u;
+            const int choice = A ? (int)lst[__ffs(A) - 1] : 0xFF;  // 0xFF: no quota left, overflow
+            // lanes with the same choice from five bit-ballots
+            const bool real = mine && choice != 0xFF;
+            const uint32_t V = __ballot_sync(0xffffffffu, real);
+            uint32_t same = V, mv = V;  // lanes choosing my option / choosing option `lane`
+#pragma unroll
+            for (int b = 0; b < 5; ++b) {
+              const uint32_t B = __ballot_sync(0xffffffffu, real && ((choice >> b) & 1));
+              same &= ((choice >> b) & 1) ? B : ~B;
+              mv &= ((lane >> b) & 1) ? B : ~B;
+            }
+            const int before = __popc(same & lt);
+            const int remc = __shfl_sync(0xffffffffu, rem_r, choice & 31);
+            const bool ok = !real || before < remc;
+            const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+            const uint32_t commit = bad ? (pending & ((1u << (__ffs(bad) - 1)) - 1u)) : pending;
+            if ((commit >> lane) & 1u) {
+              opt_s[jj] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
+              any_overflow |= choice == 0xFF;
+            }
+            rem_r -= __popc(mv & commit);  // lane v: committed lanes that chose v
+            avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
+            pending &= ~commit;
+            if (ARGUS_TAIL_TIMING && lane == 0) tail_ts[22]++;
           }
         }
       }
       __syncthreads();
-    }
-    if (warp == 0) {
-      // Serial dictatorship over a window of 32 prompts in priority order (lane = rank in
-      // the window), lane v holding rem_v.  Every pending lane takes the first option of
-      // its pi with quota left; the choices equal the sequential ones up to the first
-      // pending lane whose option earlier pending lanes used up (their count >= rem).
-      // Those lanes commit and the rest retry with the new quotas.  An option runs out at
-      // most once, so a window takes at most 1 + L steps.  A step is a handful of votes:
-      // each lane keeps the ranks (positions in its pi) still available as a bit mask A,
-      // clears the rank of each option that ran out (looked up in a per-lane inverse of
-      // pi in shared memory) and reads its choice at the lowest remaining rank.
-      uint8_t* inv = opt_s + CH + lane * 32;  // [32 lanes][32 options] rank of option v in pi, 0xFF if absent
-#pragma unroll 1
-      for (int t0 = 0; t0 < n; t0 += 32) {
-        const int jj = t0 + lane;
-        const bool act = jj < n;
-        const uint8_t* row = rk_s + (size_t)(act ? (byidx ? order_s[jj] : jj) : 0) * Lw;
-        uint32_t A = 0;  // ranks whose option has quota left
-        if (act) {
-          const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
-          for (int q = 0; q < 8; ++q) reinterpret_cast<uint32_t*>(inv)[q] = 0xFFFFFFFFu;
-          for (int q = 0; q < W; ++q) {
-            const uint32_t wq = row32[q];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const uint32_t o = (wq >> (8 * b)) & 0xFFu;
-              if (o != 0xFFu) {
-                inv[o] = (uint8_t)(4 * q + b);
-                if ((avail_r >> o) & 1u) A |= 1u << (4 * q + b);
-              }
-            }
-          }
-        }
-        __syncwarp();
-        uint32_t pending = __ballot_sync(0xffffffffu, act);
-        const uint32_t lt = (1u << lane) - 1u;
-        uint32_t seen = avail_r;  // options whose exhaustion A already reflects
-#pragma unroll 1
-        while (pending) {
-          for (uint32_t ex = seen & ~avail_r; ex; ex &= ex - 1) {  // options that ran out
-            const uint32_t r = inv[__ffs(ex) - 1];
-            if (r != 0xFFu) A &= ~(1u << r);
-          }
-          seen = avail_r;
-          const bool mine = (pending >> lane) & 1u;
-          const int choice = A ? (int)row[__ffs(A) - 1] : 0xFF;  // 0xFF: no quota left, overflow
-          // lanes with the same choice from five bit-ballots
-          const bool real = mine && choice != 0xFF;
-          const uint32_t V = __ballot_sync(0xffffffffu, real);
-          uint32_t same = V, mv = V;  // lanes choosing my option / choosing option `lane`
-#pragma unroll
-          for (int b = 0; b < 5; ++b) {
-            const uint32_t B = __ballot_sync(0xffffffffu, real && ((choice >> b) & 1));
-            same &= ((choice >> b) & 1) ? B : ~B;
-            mv &= ((lane >> b) & 1) ? B : ~B;
-          }
-          const int before = __popc(same & lt);
-          const int remc = __shfl_sync(0xffffffffu, rem_r, choice & 31);
-          const bool ok = !real || before < remc;
-          const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
-          const uint32_t commit = bad ? (pending & ((1u << (__ffs(bad) - 1)) - 1u)) : pending;
-          if ((commit >> lane) & 1u) {
-            opt_s[jj] = choice == 0xFF ? (uint8_t)0x80 : (uint8_t)choice;
-            any_overflow |= choice == 0xFF;
-          }
-          rem_r -= __popc(mv & commit);  // lane v: committed lanes that chose v
-          avail_r = __ballot_sync(0xffffffffu, lane < L && rem_r > 0);
-          pending &= ~commit;
-          if (ARGUS_TAIL_TIMING && lane == 0) tail_ts[22]++;
-        }
+      TS(15);
+      for (int t = tid; t < n; t += TT) {
+        const int i = order_s[c0 + t];
+        const int row = byidx ? i : t;
+        const int o = opt_s[t] & 0x7F;
+        uint8_t st = st_s[row];
+        if (opt_s[t] & 0x80) st |= 1u;              // ARGUS_ST_OVERFLOW (option 0)
+        if (!((cm_s[row] >> o) & 1u)) st |= 2u;     // ARGUS_ST_NONCOMPLIANT
+        a.status[i] = st;
+        a.option_out[i] = o;
       }
+      __syncthreads();
     }
-    __syncthreads();
-    TS(15);
-    for (int t = tid; t < n; t += TT) {
-      const int i = order_s[c0 + t];
-      const int row = byidx ? i : t;
-      const int o = opt_s[t] & 0x7F;
-      uint8_t st = st_s[row];
-      if (opt_s[t] & 0x80) st |= 1u;              // ARGUS_ST_OVERFLOW (option 0)
-      if (!((cm_s[row] >> o) & 1u)) st |= 2u;     // ARGUS_ST_NONCOMPLIANT
-      a.status[i] = st;
-      a.option_out[i] = o;
-    }
-    __syncthreads();
   }
   if (warp == 0 && __any_sync(0xffffffffu, any_overflow) && lane == 0) atomicOr(a.flags, FLAG_OVERFLOW);
   TS(16);
@@ -480,6 +563,21 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   const int ks_v = act ? __ldg(a.kskip + lane) : 0;
   const float gate_v = act ? __ldg(a.gate + lane) : 0.f;
   const float pth_v = act ? __ldg(a.pth + lane) : 0.f;
+  // the options' static order (init-time data): po_s[v] = position of v by (p_th desc, v asc),
+  // pg_s[v] = #{u : p_th_u > p_th_v} (equal thresholds, equal value), for A5's rank and o_i
+  __shared__ int po_s[32], pg_s[32];
+  if (warp == 0) {
+    int po = 0, pg = 0;
+#pragma unroll 8
+    for (int u = 0; u < 32; ++u) {
+      const float pu = __shfl_sync(0xffffffffu, pth_v, u);
+      const int in = u < L;
+      pg += in & (int)(pu > pth_v);
+      po += in & ((int)(pu > pth_v) | ((int)(pu == pth_v) & (int)(u < lane)));
+    }
+    po_s[lane] = po;
+    pg_s[lane] = pg;
+  }
   // layer-1 weights of this CTA's first hidden chunk (init-time data), also before the
   // predecessor finishes: B fragments of W1x, W1s and b1 columns
   constexpr int KSW = 8;  // k-steps per warp for d <= 1024: all B fragments in one round trip
@@ -520,13 +618,10 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
     __syncthreads();
   }
   TS(1);
-  // inverse norms of this warp's phase-2 prompts (0 marks an invalid prompt)
-  float iq_r[PB / TW];
-#pragma unroll
-  for (int r = 0; r < PB / TW; ++r) {
-    const int p = warp + r * TW;
-    iq_r[r] = p < nP ? __ldcg(a.inv_q + i0 + p) : 1.f;
-  }
+  // inverse norm of prompt tid of the block (0 marks an invalid prompt): K6 flags such a
+  // prompt only where it runs (the root); every rank sees the broadcast inv_q = 0, so every
+  // rank fails the call.  Loaded here, tested once the staging copies have landed.
+  const float iq = (blockIdx.y == 0 && tid < nP) ? __ldcg(a.inv_q + i0 + tid) : 1.f;
 
   // ---- stage the prompt block (16 rows of Xb; rows past N are zero padding) and the
   // block's candidate keys: list p's keys of prompts i0 .. i0 + nP - 1 are one contiguous
@@ -552,6 +647,7 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
       for (int e = lane; e < nk; e += 32) cp_async8(kst + (size_t)p * S + e, src + e);
     }
   }
+  if (iq == 0.f) atomicOr(a.flags, FLAG_INVALID_INPUT);
   cp_async_wait_all();
   __syncthreads();
   TS(2);
@@ -711,12 +807,10 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   }
   TS(8);
   // A5 for both prompts of the warp together (independent chains interleave): r_v, masks,
-  // the preference rank of v and the optimal option, from per-warp shared tables of r and
-  // p_th (broadcast reads in unrolled loops; no shuffle chains, no data-dependent branches)
+  // the preference rank of v from a per-warp shared table of r and the static option order
+  // (po_s), o_i by three warp reductions; no data-dependent branches
   constexpr int R = PB / TW;
   float* rr_s = reinterpret_cast<float*>(smraw + w2_offset(d, H) + sizeof(float) * (size_t)L * H4) + warp * R * 32;
-  float* pth_s = reinterpret_cast<float*>(smraw + w2_offset(d, H) + sizeof(float) * (size_t)L * H4) + TW * R * 32;
-  if (warp == 0) pth_s[lane] = pth_v;
   float rr[R];
   uint32_t amask[R], cmask[R];
   bool adm[R], cmp[R];
@@ -739,34 +833,34 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
   uint32_t pmask[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) pmask[r] = __ballot_sync(0xffffffffu, act && ks_v != 0 && s1_r[r] >= gate_v);
-  __syncthreads();  // rr_s of every warp, pth_s
+  __syncwarp();  // rr_s of this warp
   TS(21);
+  // rank of v in pi_i: admissible options before v by r desc, then p_th desc,
+  // then index asc -- the last two are the static order po_s
+  const int po_v = po_s[lane], pg_v = pg_s[lane];
   int rank[R], oi[R];
-  float bp[R], br[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    rank[r] = 0;
-    oi[r] = 0;
-    bp[r] = -INFINITY;
-    br[r] = -INFINITY;
-  }
-  // rank of v in pi_i: admissible options before it by (r desc, p_th desc, index asc); o_i
-  // (DESIGN R18): the compliant option with the largest p_th, then the larger
-  // r, then the lower index -- a running best over u ascending (ties keep the lower u)
+  for (int r = 0; r < R; ++r) rank[r] = 0;
 #pragma unroll 4
   for (int u = 0; u < L; ++u) {
-    const float pu = pth_s[u];
+    const uint32_t pb = (uint32_t)(po_s[u] < po_v);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const float ru = rr_s[r * 32 + u];
-      const bool before = ((amask[r] >> u) & 1u) &&
-                          (ru > rr[r] || (ru == rr[r] && (pu > pth_v || (pu == pth_v && u < lane))));
-      rank[r] += before ? 1 : 0;
-      const bool better = ((cmask[r] >> u) & 1u) && (pu > bp[r] || (pu == bp[r] && ru > br[r]));
-      bp[r] = better ? pu : bp[r];
-      br[r] = better ? ru : br[r];
-      oi[r] = better ? u : oi[r];
+      rank[r] += (int)((amask[r] >> u) & ((uint32_t)(ru > rr[r]) | ((uint32_t)(ru == rr[r]) & pb)) & 1u);
     }
+  }
+  // o_i (DESIGN R18): the compliant option with the largest p_th, then the larger
+  // r, then the lower index (r >= 0, so its bits order like the value)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool c = (cmask[r] >> lane) & 1u;
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, c ? (uint32_t)pg_v : 0xFFu);
+    const bool t1 = c && (uint32_t)pg_v == m1;
+    const uint32_t rb = __float_as_uint(rr[r]) + 1u;
+    const uint32_t m2 = __reduce_max_sync(0xffffffffu, t1 ? rb : 0u);
+    const uint32_t w = __ballot_sync(0xffffffffu, t1 && rb == m2);
+    oi[r] = w ? __ffs(w) - 1 : 0;
   }
   TS(18);
 #pragma unroll
@@ -775,9 +869,8 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
     if (p >= nP) break;
     const int i = i0 + p;
     if (act) a.rhat[(int64_t)i * L + lane] = rr[r];
-    // pi_i as a list: admissible option v at its position, 0xFF after the last
-    if (adm[r]) a.prefl[(int64_t)i * a.Lw + rank[r]] = (uint8_t)lane;
-    if (lane < a.Lw && lane >= __popc(amask[r])) a.prefl[(int64_t)i * a.Lw + lane] = 0xFF;
+    // pi_i in inverse form: rank of option v, 0xFF if v is not admissible
+    a.prefl[(int64_t)i * 32 + lane] = adm[r] ? (uint8_t)rank[r] : (uint8_t)0xFF;
     uint8_t st = (gmask != 0 && pmask[r] == 0) ? 4u /*ARGUS_ST_GATED_ALL*/ : 0u;
     if (a.policy == 1) {
       // PASM sample: u = Philox word >> 8 scaled by 2^-24 (exact), the
@@ -795,9 +888,6 @@ __global__ void __launch_bounds__(TT, 1) k_tail(TailArgs a) {
       }
     }
     if (lane == 0) {
-      // K6 flags a non-finite / zero-norm prompt only where it runs (the root); every
-      // rank sees the broadcast inv_q = 0 of that prompt, so every rank fails the call
-      if (iq_r[r] == 0.f) atomicOr(a.flags, FLAG_INVALID_INPUT);
       a.ccount[i] = (uint8_t)__popc(cmask[r]);
       a.cmask[i] = cmask[r];
       a.status[i] = st;

@@ -143,9 +143,10 @@ struct TailArgs {
   const float* pth;          // [L]
   const float* gate;         // [L]
   float delta;
-  int32_t N, d, k, H, L, Lw; // Lw = L rounded up to 4 (prefl row stride)
+  int32_t N, d, k, H, L;
   float* rhat;               // [N][L] out
-  uint8_t* prefl;            // [N][Lw] pi_i as a list: option at position r (0xFF past |A_i|)
+  uint8_t* prefl;            // [N][32] pi_i in inverse form: rank of option v (0xFF: v not admissible); 16-byte aligned
+  int32_t sd_pp_max;         // serial dictatorship one prompt per step for N <= this, else windows of 32
   uint8_t* ccount;           // [N] |C_i|
   uint32_t* cmask;           // [N] compliance mask
   // A6

@@ -96,6 +96,42 @@ __global__ void ksd(const uint8_t* rows_g, int n, int L, int Lw, const int* quot
   if (lane == 0) { out[0] = t1 - t0; out[1] = steps; }
 }
 
+// MODE 3: one prompt per step, lane v = option v: key = rank of v in pi_i (0xFF if absent)
+// when v has quota left, the choice = redux.min of (rank << 5 | v); the chain per prompt is
+// select -> redux -> compare -> decrement.
+__global__ void ksd_pp(const uint8_t* rows_g, int n, int L, int Lw, const int* quota, unsigned long long* out,
+                       int* opt_out) {
+  __shared__ uint8_t inv_s[64 * 32];
+  __shared__ uint8_t opt_s[64];
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < n * 32; i += 32) inv_s[i] = 0xFF;
+  __syncwarp();
+  for (int i = threadIdx.x; i < n * Lw; i += 32) {
+    const int p = i / Lw, r = i - p * Lw;
+    const int o = rows_g[i];
+    if (o != 0xFF) inv_s[p * 32 + o] = (uint8_t)r;
+  }
+  __syncwarp();
+  int rem = lane < L ? quota[lane] : 0;
+  const unsigned long long t0 = clock64();
+  int optr = 0;
+#pragma unroll 8
+  for (int t = 0; t < n; ++t) {
+    const uint32_t rk = inv_s[t * 32 + lane];
+    const uint32_t key = (rem > 0 && rk != 0xFFu) ? (rk << 5 | (uint32_t)lane) : 0xFFFFu;
+    const uint32_t m = __reduce_min_sync(0xffffffffu, key);
+    const int choice = m == 0xFFFFu ? 0x80 : (int)(m & 31u);
+    rem -= (choice == lane) ? 1 : 0;
+    optr = (lane == (t & 31)) ? choice : optr;
+    if ((t & 31) == 31) { opt_s[t - 31 + lane] = (uint8_t)optr; }
+  }
+  const unsigned long long t1 = clock64();
+  if (n & 31) { const int b = n & ~31; if (lane < (n & 31)) opt_s[b + lane] = (uint8_t)optr; }
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) opt_out[i] = opt_s[i];
+  if (lane == 0) { out[0] = t1 - t0; out[1] = n; }
+}
+
 int main() {
   const int n = 48, L = 12, Lw = 12;
   uint8_t rows[64 * 32];
@@ -122,6 +158,10 @@ int main() {
     cudaMemcpy(opt2, dopt, 64 * 4, cudaMemcpyDeviceToHost);
     int same = 1; for (int i = 0; i < n; ++i) same &= opt0[i] == opt2[i];
     printf("fns+min: %llu cycles, %llu steps, %.0f cycles/step, same assignment %d\n", r[0], r[1], (double)r[0] / r[1], same);
+    ksd_pp<<<1, 32>>>(drows, n, L, Lw, dq, o, dopt); cudaMemcpy(r, o, 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(opt2, dopt, 64 * 4, cudaMemcpyDeviceToHost);
+    same = 1; for (int i = 0; i < n; ++i) same &= opt0[i] == opt2[i];
+    printf("per-prompt redux.min: %llu cycles, %llu prompts, %.0f cycles/prompt, same assignment %d\n", r[0], r[1], (double)r[0] / r[1], same);
   }
   return 0;
 }

@@ -215,11 +215,21 @@ struct argus_router {
   bool pair_scan = true;           // N > 128 on CTA pairs (ARGUS_NO_PAIR=1 disables)
   int tail_ysplit = 1;             // CTAs per prompt block of a pipelined tail (ARGUS_TAIL_YSPLIT)
   int scan_reserve = 2;            // pipelined one-slice scans: SMs left to prep / tail (ARGUS_SCAN_RESERVE)
+  int scan_reserve_t = -1;         // pipelined multi-slice scans: SMs left to the previous tail (-1 = by N;
+                                   // ARGUS_SCAN_RESERVE_T)
   bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
   bool prompts_bf16 = false;       // the current call's device prompts are bf16 (argus_route_batch_bf16_dev)
   // argus_debug_capture (parity test T2): the scan also writes every exact score here
   float* dbg_scores = nullptr;
+  // diagnostics (ARGUS_SCAN_STAMP=<device address>,<launches>): the scans stamp per-CTA
+  // timestamps into a caller-owned buffer of launches x 256 CTAs x 4 u64, cyclically
+  uint32_t* d_ready = nullptr;     // pipelined one-GPU mode: last batch whose K6 completed (prep stream)
+  uint32_t ready_seq = 0;
+  bool scan_flag = false;          // one-slice scans wait for d_ready instead of a stream event (ARGUS_SCAN_FLAG=1;
+                                   // measured no gain)
+  uint64_t* stamp_buf = nullptr;
+  int64_t stamp_cap = 0, stamp_seq = 0;
   int64_t dbg_ld = 0;
   // stage profiling (argus_profile_*)
   bool prof = false;
@@ -568,7 +578,7 @@ int argus_route_destroy(argus_router* r) {
                   r->d_order, r->d_gthr[0], r->d_gthr[1], r->d_ctr[0], r->d_ctr[1], r->d_cdf, r->d_plast,
                   r->d_aff, r->d_wlist, r->d_wcount, r->d_wtime, r->d_queue, r->d_optimal, r->d_worker,
                   r->d_handle, r->d_Xasync[0], r->d_Xasync[1], r->d_Xasync[2], r->d_Xasync[3], r->d_oasync[0],
-                  r->d_oasync[1], r->d_oasync[2], r->d_oasync[3]};
+                  r->d_oasync[1], r->d_oasync[2], r->d_oasync[3], r->d_ready};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (r->h_flags) cudaFreeHost(r->h_flags);
@@ -655,6 +665,16 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   r->pair_scan = getenv("ARGUS_NO_PAIR") == nullptr;
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
   if (const char* e = getenv("ARGUS_SCAN_RESERVE")) r->scan_reserve = std::min(std::max(atoi(e), 0), 16);
+  if (const char* e = getenv("ARGUS_SCAN_FLAG")) r->scan_flag = atoi(e) != 0;
+  if (const char* e = getenv("ARGUS_SCAN_STAMP")) {
+    unsigned long long addr = 0;
+    long long cap = 0;
+    if (sscanf(e, "%llx,%lld", &addr, &cap) == 2 && addr && cap > 0) {
+      r->stamp_buf = reinterpret_cast<uint64_t*>(addr);
+      r->stamp_cap = cap;
+    }
+  }
+  if (const char* e = getenv("ARGUS_SCAN_RESERVE_T")) r->scan_reserve_t = std::min(std::max(atoi(e), -1), 32);
   r->migrate = getenv("ARGUS_NO_MIGRATE") == nullptr;
   if (r->pipe) {
     int lo = 0, hi = 0;
@@ -713,6 +733,8 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
     TRY_RC(dalloc(r, &r->d_Xb[q], (size_t)r->n_pad_max * d));
     TRY_RC(dalloc(r, &r->d_partial[q], (size_t)r->partial_lists * k));
   }
+  TRY_RC(dalloc(r, &r->d_ready, 1));
+  CU_TRY(r, cudaMemset(r->d_ready, 0, sizeof(uint32_t)));
   for (int q = 0; q < 2; ++q) {
     TRY_RC(dalloc(r, &r->d_invq[q], (size_t)r->n_pad_max));
     TRY_RC(dalloc(r, &r->d_gthr[q], (size_t)r->n_pad_max));
@@ -1061,9 +1083,15 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // C-1 (NCCL mode): rank 0's bf16 batch, inverse norms (and quotas) to every rank; in
   // pipelined mode on the comm stream, in program order with the deferred all-gathers
   cudaStream_t s_bc = (pipelined && nccl_mode(r)) ? r->comm_stream : s_scan;
+  // pipelined one-GPU one-slice scans (N <= 128, SMs reserved for prep / tail, so a scan
+  // waiting on the flag can never hold the SM K6 needs): the scan waits for a device flag
+  // the prep stream publishes instead of an event on the scan stream (k_scan_tc.cu)
+  const bool flag_wait = pipelined && r->scan_flag && !nccl_mode(r) && r->cfg.world == 1 && N <= 128 &&
+                         k > 0 && r->scan_reserve > 0;
   if (pipelined) {
+    if (flag_wait) launch_publish(r->d_ready, ++r->ready_seq, s_prep);
     CU_TRY(r, cudaEventRecord(r->ev_prep[q], s_prep));
-    CU_TRY(r, cudaStreamWaitEvent(s_bc, r->ev_prep[q], 0));
+    if (!flag_wait) CU_TRY(r, cudaStreamWaitEvent(s_bc, r->ev_prep[q], 0));
     CU_TRY(r, cudaStreamWaitEvent(r->stream, r->ev_prep[q], 0));  // the prompt buffer is consumed
   }
   r->cur = q;
@@ -1102,6 +1130,9 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   a.world = r->cfg.world;
   a.partial = r->d_partial[q];
   a.dbg = r->dbg_scores;
+  a.ready = flag_wait ? r->d_ready : nullptr;
+  a.ready_seq = r->ready_seq;
+  a.stamp = r->stamp_buf ? r->stamp_buf + (r->stamp_seq++ % r->stamp_cap) * 256 * 4 : nullptr;
   a.dbg_ld = r->dbg_ld;
   if (a.dbg && a.dbg_ld < a.m_local) return ARGUS_E_INVALID;  // capture rows too short for the shard
   a.gthr = r->d_gthr[q];
@@ -1112,7 +1143,14 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // tail run beside it instead of queueing behind the persistent grid (N = 48, fixed:
   // 264 -> 256 us per batch with 2 SMs reserved, scripts/scan_reserve_sweep.sh)
   // (pipelined NCCL mode: always, so the collectives of the neighbouring batches find SMs)
-  const int scan_sms = pipelined && (N <= 128 || nccl_mode(r)) ? r->num_sms - r->scan_reserve : r->num_sms;
+  int scan_sms = pipelined && (N <= 128 || nccl_mode(r)) ? r->num_sms - r->scan_reserve : r->num_sms;
+  if (pipelined && N > 128) {
+    // multi-slice scans are tensor-bound and fill every SM: the previous batch's tail (one
+    // CTA per 16-prompt block, one CTA per SM) would find none free until this scan ends, so
+    // a few SMs are left to it and to the next batch's prep
+    const int rt = r->scan_reserve_t >= 0 ? r->scan_reserve_t : 0;
+    scan_sms = std::min(scan_sms, r->num_sms - rt);
+  }
   {
     StageScope sc(r, ARGUS_STAGE_SCAN, s_scan);
     if (pair) {

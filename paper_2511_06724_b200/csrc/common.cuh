@@ -16,6 +16,12 @@ namespace argus {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+__device__ __forceinline__ uint64_t gtimer() {  // diagnostics stamps (ns)
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // 16-byte asynchronous global -> shared copy (LDGSTS): many in flight per thread,
 // no register round trip; cp_async_wait_all() before __syncthreads().
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

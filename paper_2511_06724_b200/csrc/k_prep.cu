@@ -105,6 +105,12 @@ __global__ void k_prep_queries(const void* __restrict__ X, int in_bf16, int N, i
   pdl_launch();
 }
 
+__global__ void k_publish(uint32_t* flag, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
+void launch_publish(uint32_t* flag, uint32_t v, cudaStream_t s) { k_publish<<<1, 1, 0, s>>>(flag, v); }
+
 void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank, int32_t world,
                         int64_t cap, bool dry, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags, cudaStream_t s) {
   if (n <= 0) return;

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int slice = blockIdx.x % slices;
   const int range = blockIdx.x / slices;  // index of this CTA's candidate list
   const int KB = KBF ? KBF : a.d / KBLK;
+  if (a.stamp != nullptr && threadIdx.x == 0) a.stamp[4 * blockIdx.x] = gtimer();
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmap_c);
@@ -140,7 +141,26 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = sm->tmem_base;
-  pdl_wait();  // setup above overlapped the previous kernel; Xb / inv_q / partial are shared
+  if (a.ready != nullptr) {
+    // pipelined one-GPU mode: nothing this scan touches is written by the previous scan
+    // (per-parity buffers); its inputs come from K6 on the prep stream, whose completion
+    // the prep stream publishes.  Waiting for that flag instead of a stream event keeps
+    // the scan stream a pure chain of scans, so this grid launches (programmatically)
+    // while the previous scan drains and each CTA starts on the SM its predecessor frees.
+    if (threadIdx.x == 0) {
+      uint32_t v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ready) : "memory");
+        if ((int32_t)(v - a.ready_seq) >= 0) break;
+        __nanosleep(128);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // K6's stores before this CTA's TMA reads
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();  // setup above overlapped the previous kernel; Xb / inv_q / partial are shared
+  }
+  if (a.stamp != nullptr && threadIdx.x == 0) a.stamp[4 * blockIdx.x + 1] = gtimer();
 
   if (warp == 0) {
     // ======================= TMA producer
@@ -269,6 +289,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (SPT != 2) tc::mma_commit_warp(tc::smem_u32(&sm->afull[b]));
     }
+    // every MMA of this CTA is issued: the next grid may be scheduled (its CTAs take the SMs
+    // this grid's CTAs free; only the drain of the last tiles and the list write remain)
+    if (a.ready != nullptr) pdl_launch();
   } else if (warp >= 4) {
     // ======================= Q into TMEM (A operand), then the epilogue
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
@@ -332,6 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t v[32];
       tc::tmem_ld32(tmem + lane_base + ACC_COL0 + b * TN + h * 32, v);
       tc::tmem_wait_ld();
+      if (a.stamp != nullptr && l == 0 && warp == 4 && lane == 0) a.stamp[4 * blockIdx.x + 2] = gtimer();
       // Release accumulator b right away so MMA(l+2) never waits for this tile's
       // processing.  inv_c slot l % 8 stays valid: the producer refills it for tile
       // l+8 only after done(l+6), which needs every epilogue warp's release of tile
@@ -374,6 +398,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   tc::fence_before();
   __syncthreads();
+  if (a.stamp != nullptr && threadIdx.x == 0) a.stamp[4 * blockIdx.x + 3] = gtimer();
   pdl_launch();
   if (warp == 2) {
     tc::fence_after();

@@ -53,6 +53,12 @@ struct ScanArgs {
   int32_t home_max;          // pair scan: home pairs per pair slice = their list slots [0, home_max)
   int32_t floaters;          // pair scan: pairs beyond home_max * pair slices (slots home_max + f)
   int32_t grid_ctas;         // pair scan with migration: CTAs launched (all SMs' pairs)
+  const uint32_t* ready;     // pipelined one-GPU one-slice scans: wait until *ready - ready_seq >= 0
+                             // (the prep stream publishes it after K6) instead of a stream event + the
+                             // grid-dependency wait; NULL: griddepcontrol.wait
+  uint32_t ready_seq;
+  uint64_t* stamp;           // diagnostics (ARGUS_SCAN_STAMP): per CTA %globaltimer at entry, after the
+                             // grid-dependency wait, first accumulator read, exit (NULL: off)
   float* dbg;                // argus_debug_capture: every exact score to dbg[p * dbg_ld + slot] (NULL: off)
   int64_t dbg_ld;
 };
@@ -64,6 +70,9 @@ constexpr int MAX_VISITS = 4;   // migrant pairs per pair slice (list slots home
 // g % world == rank go to slot g / world.
 void launch_insert_rows(const float* rows, int64_t n, int64_t g0, int32_t d, int32_t rank, int32_t world,
                         int64_t cap, bool dry, __nv_bfloat16* Cb, float* inv_c, uint32_t* flags, cudaStream_t s);
+
+// Publishes v into *flag (release, gpu scope) once the stream's earlier work is complete.
+void launch_publish(uint32_t* flag, uint32_t v, cudaStream_t s);
 
 // K6: prompts fp32 [N][d] -> Xb bf16 [n_pad][d] (zero padded), inv_q [n_pad].
 // With quota != nullptr (host [L]) it also writes the quotas into quota_dev [32]

@@ -240,6 +240,23 @@ def cpu_baseline(cfg, cache_rows, queries, opts, W1, b1, W2, b2, quota_fn, secon
                            "sample": f"{S1} prompts scanned (O1-O4) over the full cache on 1 thread; {wall1:.1f} s wall"}}
 
 
+def workload_config(cfg, sizes, fixed_n, world):
+    """The `config` object of the JSON line: the workload only, identical in both arms
+    (this one and --impl reference); how the run executed goes under "run"."""
+    opts = gen.option_table(cfg.models, cfg.ks)
+    shard = -(-cfg.M // world) * (2 * cfg.d + 4)
+    return {
+        "workload": f"{cfg.name}: {cfg.note}",
+        "M": cfg.M, "d": cfg.d, "k": cfg.k, "L": len(opts), "hidden": cfg.hidden,
+        "batch_sizes": (f"MMPP trace seed 2018, {len(sizes)} batches (mean N {np.mean(sizes):.1f}, min {min(sizes)}, "
+                        f"max {max(sizes)}); timed steps: whole trace passes, then the contiguous window of the "
+                        f"trace closest to it in mean N and high-state share") if (cfg.bursty and not fixed_n)
+                       else f"N={sizes[0]} ({len(sizes)} distinct batches cycled)",
+        "l2": (f"inputs larger than L2 (cache shard {shard / 1e9:.2f} GB >> 126 MB L2)" if shard > 126e6
+               else f"cache shard {shard / 1e6:.1f} MB fits in L2 (parity-size workload, not a roofline line)"),
+    }
+
+
 def cpu_model():
     """`lscpu` model name of this host (from /proc/cpuinfo)."""
     try:
@@ -514,16 +531,10 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {
-            "workload": f"{cfg.name}: {cfg.note}",
-            "M": cfg.M, "d": d, "k": k, "L": L, "hidden": cfg.hidden,
-            "batch_sizes": (f"MMPP trace seed 2018, {NT} batches (mean N {np.mean(sizes):.1f}, min {min(sizes)}, "
-                            f"max {max(sizes)}); timed steps: whole trace passes, then the contiguous window of the "
-                            f"trace closest to it in mean N and high-state share") if (cfg.bursty and not args.fixed_n)
-                           else f"N={sizes[0]} ({NT} distinct batches cycled)",
+        "config": workload_config(cfg, sizes, args.fixed_n, world),
+        "run": {
             "timed_batches": timed_n,
             "parallelism": f"cache row-striped over {world} GPU(s)",
-            "l2": f"inputs larger than L2 (cache shard {bytes_per_launch / 1e9:.2f} GB >> 126 MB L2)",
             "insert_s": round(t_insert, 2),
             "pipeline": (("tail of batch b overlaps the scan of batch b+1 (argus_config.pipeline=1); every "
                           "batch's outputs are complete inside the timed region")
@@ -704,8 +715,8 @@ def run_reference(args, cfg, rank, world):
         "value": round(value, 3), "unit": "prompts/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.note}", "M": cfg.M, "d": d, "k": k, "L": L,
-                   "sample_per_step": sample},
+        "config": workload_config(cfg, sizes, 0, world),
+        "run": {"sample_per_step": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "prompts/s", "cores": threads, "kind": "oracle",
                          "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "prompts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

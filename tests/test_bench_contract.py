@@ -22,6 +22,12 @@ def test_reference_arm_json_line():
     assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] >= 1
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in j["config"]
+    # the same workload object the product arm prints (driver: same_config)
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import argus_inputs as gen
+    cfg = gen.CONFIGS["C1"]
+    assert j["config"] == bench.workload_config(cfg, bench.batch_sizes(cfg, bench.n_trace(cfg)), 0, 1)
 
 
 def test_product_bench_refuses_without_gpu():

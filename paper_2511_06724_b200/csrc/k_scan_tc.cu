@@ -37,7 +37,8 @@
 #include "scan_epi.cuh"
 
 #ifndef ARGUS_SCAN_EXP
-#define ARGUS_SCAN_EXP 0  // diagnostics only: 1 = skip epilogue math, 2 = skip MMAs (tools/scan_experiments.sh)
+#define ARGUS_SCAN_EXP 0  // diagnostics only: 1 = skip epilogue math, 2 = skip MMAs (tools/scan_experiments.sh),
+                          // 3 = M = 64 MMAs, 4 = half the k-steps (scripts/r02_power_exp2.sh)
 #endif
 
 namespace argus {
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // commits) is slower than the 32 cycles an M=128 N=64 K=16 MMA executes in; two
     // interleaved issuers keep the tensor pipe fed.  tcgen05.commit tracks the MMAs
     // of the committing thread only, so the two barrier sets stay independent.
-    constexpr uint32_t IDESC = tc::idesc_bf16_f32(TM, TN);
+    // diagnostics (scores wrong): ARGUS_SCAN_EXP = 3 issues M = 64 MMAs, = 4 half of the k-steps
+    constexpr uint32_t IDESC = tc::idesc_bf16_f32(ARGUS_SCAN_EXP == 3 ? 64 : TM, TN);
     tc::mbar_wait(tc::smem_u32(&sm->qready), 0);
     if (KBV > KB_TMEM) tc::mbar_wait(tc::smem_u32(&sm->atail), 0);
     tc::fence_after();
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (KBV == KB_TMEM || kb < KB_TMEM) {
 #pragma unroll
             for (int kk = 0; kk < KBLK / 16; ++kk)
-              if (ARGUS_SCAN_EXP != 2 || (kb | kk) == 0)
+              if ((ARGUS_SCAN_EXP != 2 || (kb | kk) == 0) && (ARGUS_SCAN_EXP != 4 || (kk & 1) == 0))
                 tc::mma_ts_warp(d_tmem, tmem + (uint32_t)((kb * (KBLK / 16) + kk) * 8),
                                 dslot + (uint64_t)((j * BOX_BYTES + kk * 32) >> 4), IDESC, (kb | kk) != 0);
           } else {  // A tail from shared memory (same SW128 K-major layout as the TMA box)

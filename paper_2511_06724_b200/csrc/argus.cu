@@ -219,6 +219,8 @@ struct argus_router {
                                    // ARGUS_SCAN_RESERVE_T)
   bool migrate = true;             // pair scan: pairs migrate to unfinished slices (ARGUS_NO_MIGRATE=1 disables)
   CUtensorMap tmap_q[2];           // TMA descriptors of the bf16 prompt batches (64x128 boxes, SW128)
+  CUtensorMap tmap_q16[2];         // same batches, 64x16 boxes (the transposed small-N scan's B operand)
+  bool scan_t = false;             // N <= 64: transposed scan with exact tensor work (ARGUS_SCAN_T)
   bool prompts_bf16 = false;       // the current call's device prompts are bf16 (argus_route_batch_bf16_dev)
   // argus_debug_capture (parity test T2): the scan also writes every exact score here
   float* dbg_scores = nullptr;
@@ -666,6 +668,7 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (const char* e = getenv("ARGUS_TAIL_YSPLIT")) r->tail_ysplit = atoi(e);
   if (const char* e = getenv("ARGUS_SCAN_RESERVE")) r->scan_reserve = std::min(std::max(atoi(e), 0), 16);
   if (const char* e = getenv("ARGUS_SCAN_FLAG")) r->scan_flag = atoi(e) != 0;
+  if (const char* e = getenv("ARGUS_SCAN_T")) r->scan_t = atoi(e) != 0;
   if (const char* e = getenv("ARGUS_SCAN_STAMP")) {
     unsigned long long addr = 0;
     long long cap = 0;
@@ -793,7 +796,9 @@ int argus_route_init(const argus_config* cfg, const argus_option* opts, const fl
   if (!make_tmap(&r->tmap_c, r->d_Cb, r->cap_local + 256, d, 64) ||
       !make_tmap(&r->tmap_c32, r->d_Cb, r->cap_local + 256, d, 32) ||
       !make_tmap(&r->tmap_q[0], r->d_Xb[0], r->n_pad_max, d, 128) ||
-      !make_tmap(&r->tmap_q[1], r->d_Xb[1], r->n_pad_max, d, 128)) {
+      !make_tmap(&r->tmap_q[1], r->d_Xb[1], r->n_pad_max, d, 128) ||
+      !make_tmap(&r->tmap_q16[0], r->d_Xb[0], r->n_pad_max, d, 16) ||
+      !make_tmap(&r->tmap_q16[1], r->d_Xb[1], r->n_pad_max, d, 16)) {
     argus_route_destroy(r);
     return ARGUS_E_CUDA;
   }
@@ -1185,7 +1190,11 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
         if (getenv("ARGUS_DEBUG")) fprintf(stderr, "argus: CTA-pair scan unavailable, using one slice per CTA\n");
       }
     }
-    if (!pair) {
+    if (!pair && r->scan_t && scan_t_supported(d, N, k)) {
+      a.P = scan_t_plan_ranges(a.m_local, scan_sms);
+      if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;
+      if (launch_scan_t(a, &r->tmap_c, &r->tmap_q16[q], s_scan, true) != cudaSuccess) return ARGUS_E_CUDA;
+    } else if (!pair) {
       a.P = scan_plan_ranges(a.m_local, N, scan_sms);
       if ((int64_t)a.P * N > r->partial_lists) return ARGUS_E_STATE;
       launch_scan(a, &r->tmap_c, &r->tmap_q[q], s_scan, true);

@@ -86,6 +86,13 @@ void launch_prep_queries(const void* X, bool in_bf16, int32_t N, int32_t n_pad, 
                          bool pdl = true, const int32_t* quota = nullptr, int32_t L = 0,
                          int32_t* quota_dev = nullptr);
 
+// K1+K2 for N <= 64 prompts (d = 768, k <= 8), transposed: cache rows are the MMA's M, the
+// prompts its N (k_scan_t.cu).  a.P = CTAs = candidate lists (scan_t_plan_ranges).
+bool scan_t_supported(int d, int32_t N, int k);
+int scan_t_plan_ranges(int64_t m_local, int num_sms);
+cudaError_t launch_scan_t(const ScanArgs& a, const CUtensorMap* tmap_c, const CUtensorMap* tmap_q16, cudaStream_t s,
+                          bool pdl);
+
 // K1+K2: fused tcgen05 scan + per-range top-k -> partial [P][N][k].
 // scan_plan_ranges returns P (cache ranges; grid = P * ceil(N / 128) CTAs).
 int scan_plan_ranges(int64_t m_local, int32_t N, int num_sms);

@@ -11,11 +11,15 @@
 //
 // Roles: warp 0 = TMA producer (prompts once, then 128-row cache tiles one k-block per ring
 // slot), warp 1 = MMA issuer, warp 2 = TMEM allocator, warps 4..7 = row warps (TMEM lane
-// quarter q: cache rows 32q .. 32q+31 of the tile), warps 8..9 = column warps (lane = prompt:
+// quarter q: cache rows 32q .. 32q+31 of the tile), warps 8..11 = column warps (lane = prompt:
 // the per-prompt top-k in registers).  Per tile the row warps read the accumulator (lane =
 // cache row, column = prompt) and park the raw fp32 values transposed in shared memory, 64
 // rows at a time; the column warps then run k_scan_tc's chunk epilogue (epi_chunk) on 32-row
 // chunks of their prompt's column -- the same code, the same bound filter, the same keys.
+//
+// Measured (DESIGN.md §9 item 0, profiles/r02/sched/scan_t/): parity-green, mainloop 7.08 TB/s
+// at N = 48 (+3 % over k_scan_tc) but slower overall with the column epilogue, so it is opt-in
+// (ARGUS_SCAN_T=1) and k_scan_tc serves N <= 128 by default.
 #include <cstddef>
 #include <cstdlib>
 
@@ -37,7 +41,8 @@ constexpr int KBLK = 64;                     // bf16 per 128-byte swizzle row
 constexpr int KB = 12;                       // k-blocks (d = 768)
 constexpr int SLOT_BYTES = TR * KBLK * 2;    // one k-block of a tile: two 64-row boxes, 16 KB
 constexpr int NP_MAX = 64;                   // prompts (UMMA N) at most
-constexpr int THREADS = 320;                 // 4 control + 4 row + 2 column warps
+constexpr int THREADS = 384;                 // 4 control + 4 row + 4 column warps
+constexpr int COLW = 4;                      // column warps: 2 prompt groups x 2 row chunks
 constexpr int INV_SLOTS = 8;
 constexpr int CHUNK = 4;                     // tiles per dynamically scheduled work unit
 constexpr int TSTRIDE = 64 + 4;              // transposed half tile: [prompt][64 rows], padded
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* ttile = reinterpret_cast<float*>(base + bbytes + (size_t)nsl * SLOT_BYTES);  // [NP][TSTRIDE]
   uint8_t* after = reinterpret_cast<uint8_t*>(ttile) + sizeof(float) * (size_t)NP_MAX * TSTRIDE;
   const uint32_t scratch0 = tc::smem_u32(after);  // 2 column warps x 16 x 32 fp32
-  TSmem* sm = reinterpret_cast<TSmem*>(after + 2 * 16 * 32 * 4);
+  TSmem* sm = reinterpret_cast<TSmem*>(after + COLW * 16 * 32 * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int range = blockIdx.x;  // one slice: CTA = candidate list
 
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::mbar_init(tc::smem_u32(&sm->bfull), 1);
     for (int s = 0; s < INV_SLOTS; ++s) {
       tc::mbar_init(tc::smem_u32(&sm->invfull[s]), 1);
-      tc::mbar_init(tc::smem_u32(&sm->invempty[s]), 2 * 32);
+      tc::mbar_init(tc::smem_u32(&sm->invempty[s]), COLW * 32);
     }
     tc::fence_barrier_init();
   }
@@ -211,18 +216,21 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < 32; ++c) ttile[(32 + c) * TSTRIDE + r] = __uint_as_float(v1[c]);
           }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(6 * 32) : "memory");  // stored
-        asm volatile("bar.sync 2, %0;" ::"n"(6 * 32) : "memory");  // read
+        asm volatile("bar.sync 1, %0;" ::"n"(8 * 32) : "memory");  // stored
+        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // read
       }
     }
   } else if (warp >= 8) {
-    // ======================= column warps: lane = prompt, the per-prompt top-k
-    const int p = (warp - 8) * 32 + lane;  // prompt
+    // ======================= column warps: lane = prompt, the per-prompt top-k; warp cw takes
+    // prompts 32 (cw & 1) .. + 31 and row chunk cw >> 1 of every half tile (two lists per
+    // prompt, folded at the end)
+    const int cw = warp - 8, chs = cw >> 1;
+    const int p = (cw & 1) * 32 + lane;  // prompt
     const bool active = p < a.N;
     tc::mbar_wait(tc::smem_u32(&sm->bfull), 0);
     const float iq = active ? a.inv_q[p] : 0.f;
-    const bool live = (warp - 8) * 32 < NP;  // warp has prompts at all
-    const uint32_t scratch = scratch0 + (uint32_t)((warp - 8) * 16 * 32 * 4);
+    const bool live = (cw & 1) * 32 < NP;  // warp has prompts at all
+    const uint32_t scratch = scratch0 + (uint32_t)(cw * 16 * 32 * 4);
     TopList<KMAX> tl;
     tl.clear();
     float thr = active ? -INFINITY : INFINITY;
@@ -236,10 +244,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (t < 0) break;
       if (gk != 0) thr = fmaxf(thr, key_score(gk));
       for (int hh = 0; hh < 2; ++hh) {
-        asm volatile("bar.sync 1, %0;" ::"n"(6 * 32) : "memory");  // the half tile is stored
+        asm volatile("bar.sync 1, %0;" ::"n"(8 * 32) : "memory");  // the half tile is stored
         if (live && ARGUS_SCANT_EXP == 0) {
-#pragma unroll 1
-          for (int ch = 0; ch < 2; ++ch) {
+          {
+            const int ch = chs;
             const int r0 = ch * 32;                          // rows r0 .. r0+31 of the half
             const int64_t j0 = t * TR + hh * 64 + r0;       // local cache row of the chunk
             uint32_t v[32];
@@ -264,12 +272,21 @@ __global__ void __launch_bounds__(THREADS, 1)
             atomicMax(reinterpret_cast<unsigned long long*>(gthr_p), (unsigned long long)published);
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"n"(6 * 32) : "memory");  // the half tile is read
+        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // the half tile is read
       }
       if (active && (l & 3) == 3) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
       tc::mbar_arrive(tc::smem_u32(&sm->invempty[li]));  // inv_c slot l % 8 free
     }
-    if (active) {
+    // fold the two chunk lists of each prompt (the transposed tile is idle now)
+    uint64_t* xchg = reinterpret_cast<uint64_t*>(ttile) + (size_t)((cw & 1) * 32 + lane) * KMAX;
+    if (chs == 1) {
+#pragma unroll
+      for (int t2 = 0; t2 < KMAX; ++t2) xchg[t2] = tl.v[t2];
+    }
+    asm volatile("bar.sync 3, %0;" ::"n"(COLW * 32) : "memory");
+    if (chs == 0 && active) {
+#pragma unroll
+      for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(xchg[t2]);
       uint64_t* out = a.partial + ((int64_t)range * a.N + p) * a.k;
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2)
@@ -290,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Shared memory of a launch with np prompts (B) and nsl ring slots.
 static size_t smem_bytes(int np, int nsl) {
   return 1024 + (size_t)KB * np * 128 + (size_t)nsl * SLOT_BYTES + sizeof(float) * NP_MAX * TSTRIDE +
-         2 * 16 * 32 * 4 + sizeof(TSmem);
+         COLW * 16 * 32 * 4 + sizeof(TSmem);
 }
 
 bool scan_t_supported(int d, int32_t N, int k) { return d == KB * KBLK && N >= 1 && N <= NP_MAX && k >= 1 && k <= 8; }

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Transposed small-N scan (ARGUS_SCAN_T=1): parity first (short timeouts), then A/B.
 set -u
-OUT=gpurun_out/scant
+OUT=gpurun_out/scant${SUFFIX:-}
 mkdir -p $OUT
 python -m paper_2511_06724_b200.build > $OUT/build.log 2>&1 || { cat $OUT/build.log; exit 1; }
 export ARGUS_SCAN_T=1

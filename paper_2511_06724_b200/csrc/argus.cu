@@ -1091,8 +1091,9 @@ static int partial_impl(argus_router* r, const float* prompts_dev, int32_t N, ui
   // pipelined one-GPU one-slice scans (N <= 128, SMs reserved for prep / tail, so a scan
   // waiting on the flag can never hold the SM K6 needs): the scan waits for a device flag
   // the prep stream publishes instead of an event on the scan stream (k_scan_tc.cu)
+  // (k_scan_tc only: the opt-in transposed scan keeps the event + grid-dependency wait)
   const bool flag_wait = pipelined && r->scan_flag && !nccl_mode(r) && r->cfg.world == 1 && N <= 128 &&
-                         k > 0 && r->scan_reserve > 0;
+                         k > 0 && r->scan_reserve > 0 && !(r->scan_t && scan_t_supported(d, N, k));
   if (pipelined) {
     if (flag_wait) launch_publish(r->d_ready, ++r->ready_seq, s_prep);
     CU_TRY(r, cudaEventRecord(r->ev_prep[q], s_prep));

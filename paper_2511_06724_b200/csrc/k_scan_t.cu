@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t bbytes = (uint32_t)(KB * NP * 128);
   const uint32_t ring_s = b_s + bbytes;
   float* ttile = reinterpret_cast<float*>(base + bbytes + (size_t)nsl * SLOT_BYTES);  // [NP][TSTRIDE]
-  uint8_t* after = reinterpret_cast<uint8_t*>(ttile) + sizeof(float) * (size_t)NP_MAX * TSTRIDE;
+  uint8_t* after = reinterpret_cast<uint8_t*>(ttile) + 2 * sizeof(float) * (size_t)NP_MAX * TSTRIDE;  // 2 halves
   const uint32_t scratch0 = tc::smem_u32(after);  // 2 column warps x 16 x 32 fp32
   TSmem* sm = reinterpret_cast<TSmem*>(after + COLW * 16 * 32 * 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int half = q >> 1;                             // rows 0..63 (half 0) or 64..127
     const int r = (q & 1) * 32 + lane;                   // row within the half
-    for (int64_t l = 0;; ++l) {
+    int64_t l = 0;
+    for (;; ++l) {
       tc::mbar_wait(tc::smem_u32(&sm->invfull[l & (INV_SLOTS - 1)]), (uint32_t)((l >> 3) & 1));
       if (sm->tile_id[l & (INV_SLOTS - 1)] < 0) break;
       const int b = (int)(l & 1);
@@ -206,19 +207,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::tmem_wait_ld();
       tc::fence_before();
       tc::mbar_arrive(tc::smem_u32(&sm->tempty[b]));
+      // half hh goes to buffer hh (named barriers 1 + hh: stored, 3 + hh: read); the row warps
+      // wait only for the column warps' release of the same half of the previous tile, so
+      // they store half 1 while the column warps work through half 0
       for (int hh = 0; hh < 2; ++hh) {
-        // half hh: its two row warps store, the column warps read (bar 1 = 6 warps)
+        float* tb = ttile + (size_t)hh * NP_MAX * TSTRIDE;
+        if (l > 0) asm volatile("bar.sync %0, %1;" ::"r"(3 + hh), "n"(8 * 32) : "memory");
         if (half == hh && ARGUS_SCANT_EXP < 2) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) ttile[c * TSTRIDE + r] = __uint_as_float(v0[c]);
+          for (int c = 0; c < 32; ++c) tb[c * TSTRIDE + r] = __uint_as_float(v0[c]);
           if (NP > 32) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) ttile[(32 + c) * TSTRIDE + r] = __uint_as_float(v1[c]);
+            for (int c = 0; c < 32; ++c) tb[(32 + c) * TSTRIDE + r] = __uint_as_float(v1[c]);
           }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(8 * 32) : "memory");  // stored
-        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // read
+        asm volatile("bar.arrive %0, %1;" ::"r"(1 + hh), "n"(8 * 32) : "memory");
       }
+    }
+    // balance the column warps' releases of the last tile (none if this CTA got no tile)
+    if (l > 0) {
+      asm volatile("bar.sync 3, %0;" ::"n"(8 * 32) : "memory");
+      asm volatile("bar.sync 4, %0;" ::"n"(8 * 32) : "memory");
     }
   } else if (warp >= 8) {
     // ======================= column warps: lane = prompt, the per-prompt top-k; warp cw takes
@@ -244,14 +253,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (t < 0) break;
       if (gk != 0) thr = fmaxf(thr, key_score(gk));
       for (int hh = 0; hh < 2; ++hh) {
-        asm volatile("bar.sync 1, %0;" ::"n"(8 * 32) : "memory");  // the half tile is stored
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + hh), "n"(8 * 32) : "memory");  // half hh stored
+        const float* tb = ttile + (size_t)hh * NP_MAX * TSTRIDE;
         if (live && ARGUS_SCANT_EXP == 0) {
           {
             const int ch = chs;
             const int r0 = ch * 32;                          // rows r0 .. r0+31 of the half
             const int64_t j0 = t * TR + hh * 64 + r0;       // local cache row of the chunk
             uint32_t v[32];
-            const float* col = ttile + (p < NP ? p : 0) * TSTRIDE + r0;
+            const float* col = tb + (p < NP ? p : 0) * TSTRIDE + r0;
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 f = *reinterpret_cast<const float4*>(col + j);
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             atomicMax(reinterpret_cast<unsigned long long*>(gthr_p), (unsigned long long)published);
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"n"(8 * 32) : "memory");  // the half tile is read
+        asm volatile("bar.arrive %0, %1;" ::"r"(3 + hh), "n"(8 * 32) : "memory");  // half hh read
       }
       if (active && (l & 3) == 3) gk = __ldcg(reinterpret_cast<const unsigned long long*>(gthr_p));
       tc::mbar_arrive(tc::smem_u32(&sm->invempty[li]));  // inv_c slot l % 8 free
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2) xchg[t2] = tl.v[t2];
     }
-    asm volatile("bar.sync 3, %0;" ::"n"(COLW * 32) : "memory");
+    asm volatile("bar.sync 5, %0;" ::"n"(COLW * 32) : "memory");
     if (chs == 0 && active) {
 #pragma unroll
       for (int t2 = 0; t2 < KMAX; ++t2) tl.insert(xchg[t2]);
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 // Shared memory of a launch with np prompts (B) and nsl ring slots.
 static size_t smem_bytes(int np, int nsl) {
-  return 1024 + (size_t)KB * np * 128 + (size_t)nsl * SLOT_BYTES + sizeof(float) * NP_MAX * TSTRIDE +
+  return 1024 + (size_t)KB * np * 128 + (size_t)nsl * SLOT_BYTES + 2 * sizeof(float) * NP_MAX * TSTRIDE +
          COLW * 16 * 32 * 4 + sizeof(TSmem);
 }
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # k_scan_t with the row-layout epilogue: its parity tests, then A/B against k_scan_tc.
 set -u
-OUT=gpurun_out/scant2
+OUT=gpurun_out/scant${SUFFIX:-2}
 mkdir -p $OUT
 python -m paper_2511_06724_b200.build > $OUT/build.log 2>&1 || { cat $OUT/build.log; exit 1; }
 timeout 300 python -m pytest tests/test_gpu_scan_t.py -x -q -p no:cacheprovider > $OUT/pytest_scan_t.log 2>&1; echo "rc=$?" >> $OUT/pytest_scan_t.log
